@@ -1,0 +1,372 @@
+#!/usr/bin/env python3
+"""bench.py -- α-grid replay throughput of Marconi's hybrid prefix cache on B200.
+
+Metric (BASELINE.json): "requests replayed/sec × α-candidates at 1/2/4/8 B200;
+HBM GB/s vs peak".  Workload: BASELINE.json configs[2] -- the ShareGPT-shaped
+50k-request trace, 7B hybrid {4,24,28}, 60 GB cache, 16-value α grid x 128
+trace segments = 2,048 chains, sharded over N GPUs (strong scaling: the same
+chain list at every N).  A step = one replay of every chain of this rank's
+shard from its segment snapshot + the NCCL all-gather of per-α hit sums + α*
+selection.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3]
+
+Setup (untimed, reported): trace generation, H2D, the α = 0 device live pass
+that produces the 128 segment snapshots.  L2 is flushed (a 256 MiB write)
+between timed steps, outside the per-step CUDA-event window.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "requests replayed/sec×α-candidates at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "request-replays/s"
+# algorithmic bytes per request-replay:
+#   B_r = 8*c_r + 16*v_r + 13*sum_j N_j + 32*w_r + 16
+W_CMP, W_VIS, W_SCAN, W_WR, W_OUT = 8, 16, 13, 32, 16
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", type=int, default=3)
+    p.add_argument("--requests", type=int, default=0, help="override R (testing only)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="target wall time of the oracle sample")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def algorithmic_bytes(ctr: np.ndarray, n_req_replayed: int) -> int:
+    c = ctr.astype(np.int64).sum(0)
+    return int(W_CMP * c[0] + W_VIS * c[1] + W_SCAN * c[2] + W_WR * c[3] + W_OUT * n_req_replayed)
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle arms (the only places bench.py executes oracle/)
+# ----------------------------------------------------------------------------
+def oracle_sample(w, target_s: float, cores: int):
+    """A bounded sample of the same workload for the oracle: the first k segments x all α,
+    with k sized so the sample takes about target_s seconds on `cores` threads."""
+    import oracle as O
+    tr, v = w.trace, w.variants[0]
+    W = w.window
+    # calibrate: single-thread time per request-replay on one α = 1 chain of segment 1
+    snaps, *_ = O.live_pass(tr, v, W, upto=W)
+    t0 = time.perf_counter()
+    O.run_chains(tr, [v], [(0, 1.0, W + 1, W, 1)], snaps, n_threads=1) if len(snaps) > 1 else None
+    per_req = max((time.perf_counter() - t0) / W, 1e-6)
+    na = len(w.alphas)
+    k = int(max(1, min(len(w.segments()), target_s * cores / (per_req * W * na))))
+    snaps, *_ = O.live_pass(tr, v, W, upto=min(k * W, tr.n_requests))
+    segs = w.segments()[:k]
+    chains = [(0, a, f, n, i) for a in w.alphas for i, (f, n) in enumerate(segs)]
+    return snaps, chains
+
+
+def run_oracle(w, snaps, chains, cores):
+    import oracle as O
+    t0 = time.perf_counter()
+    hit, fl, by, hs, ctr = O.run_chains(w.trace, [w.variants[0]], chains, snaps, n_threads=cores)
+    dt = time.perf_counter() - t0
+    n = sum(c[3] for c in chains)
+    return n, dt
+
+
+def cpu_baseline(w, target_s):
+    cores = os.cpu_count() or 1
+    snaps, chains = oracle_sample(w, target_s, cores)
+    n, dt = run_oracle(w, snaps, chains, cores)
+    k = len(snaps)
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {k} of {len(w.segments())} segments x {len(w.alphas)} alphas = {len(chains)} chains, "
+                      f"{n} request-replays in {dt:.2f} s (snapshots from the oracle's own live pass, untimed)"}
+
+
+def reference_arm(args, w, config):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    snaps, chains = oracle_sample(w, min(args.cpu_seconds, 8.0), cores)
+    for _ in range(args.warmup):
+        run_oracle(w, snaps, chains, cores)
+    tot_n, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        n, dt = run_oracle(w, snaps, chains, cores)
+        tot_n += n
+        tot_t += dt
+    v = tot_n / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64+f64",
+            "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{len(chains)} chains of the first {len(snaps)} segments per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# B200 arm
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    import tracegen as tg
+    t_gen = time.perf_counter()
+    w = tg.workload(args.config, R=args.requests or None)
+    t_gen = time.perf_counter() - t_gen
+    tr = w.trace
+    config = {"workload": f"config{args.config} {w.name}-shaped trace, {tr.n_requests} requests, "
+                          f"{len(w.variants)} cache variant(s), {len(w.alphas)} alphas x {len(w.segments())} "
+                          f"segments = {w.n_chains} chains",
+              "requests": tr.n_requests, "tokens": tr.n_tokens, "alphas": len(w.alphas),
+              "segments": len(w.segments()), "chains": w.n_chains, "window": w.window,
+              "model": "7B hybrid {4 attn, 24 ssm, 28 mlp}, D=4096, N=128, fp16" if args.config in (2, 3, 4)
+              else "see tracegen.workload", "cache_bytes": [v.capacity_bytes for v in w.variants],
+              "l2": "flushed (256 MiB write) between timed steps, outside the event window"}
+    if args.impl == "reference":
+        return reference_arm(args, w, config)
+
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2411_19379_b200 import AlphaGrid
+    from paper_2411_19379_b200 import marconi as M
+
+    t_setup = time.perf_counter()
+    g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments, rank=rank, world=world, device=local)
+    g.setup()
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+    out = g.ctx.alloc_outputs(len(w.alphas), counters=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    my_reqs = int(sum(g.segs[c % len(g.segs)][1] for c in g.chains))
+    all_reqs = sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants)
+
+    def step():
+        out["hit_sum"].zero_()
+        g.run(out=out)
+        return g.select(out)
+
+    for _ in range(args.warmup):
+        step()
+    g.ctx.check()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    step_ms, kern_ms = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out["hit_sum"].zero_()
+        g.run(out=out)               # replay_kernel on `stream`
+        e1.record(stream)
+        a_star = g.select(out)       # D2H + all-gather + argmax
+        e2.record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e2))
+        kern_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    g.ctx.check()
+    tot = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    T_ms, K_ms = float(tot[0]), float(tot[1])
+    value = all_reqs * args.steps / (T_ms / 1000.0)
+
+    # roofline of the dominant kernel (replay_kernel) from the device counters of this rank
+    ctr = out["counters"].cpu().numpy()[g.chains.astype(np.int64)]
+    alg_bytes = algorithmic_bytes(ctr, my_reqs)
+    kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1000.0
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / kern_avg_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "replay_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            if tj.get("config") == args.config and tj.get("n_gpus", 1) == world:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e through the public API with host buffers (rank-local shard)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(g, w, args, out)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": T_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+            "config": dict(config, parallelism=f"chains sharded over {world} GPU(s) (LPT), NCCL all-gather of "
+                                                 f"per-alpha hit sums", alpha_star=a_star,
+                           setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "replay_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "launch_ms": kern_avg_s * 1000.0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,  # one replay_kernel launch per step
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(g, w, args, out):
+    """Same metric end to end through the C ABI from pinned host buffers: per step H2D of the trace
+    (tokens + requests) and the segment snapshots, the replay, D2H of per-request hits and hit sums."""
+    import torch
+    from paper_2411_19379_b200 import marconi as M
+    tr = w.trace
+    ctx = g.ctx
+    h_tok = torch.from_numpy(np.ascontiguousarray(tr.tokens, np.uint32).view(np.int32)).pin_memory()
+    h_req = torch.from_numpy(M.requests_array(tr.off, tr.lin, tr.lout).view(np.int64)).pin_memory()
+    snaps = [ctx.get_snapshot(0, k) for k in range(ctx.snapshot_count(0))]
+    d_tok = torch.empty_like(h_tok, device="cuda")
+    d_req = torch.empty_like(h_req, device="cuda")
+    h_hit = torch.empty(out["hit"].shape, dtype=torch.int32).pin_memory()
+    snap_bytes = sum(len(s[0]) for s in snaps) * M.SNAP_DTYPE.itemsize
+    h2d = h_tok.numel() * 4 + h_req.numel() * 8 + snap_bytes
+    d2h = h_hit.numel() * 4 + out["hit_sum"].numel() * 8
+    stream = torch.cuda.current_stream()
+    n_units = sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants)
+
+    def one():
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_req.copy_(h_req, non_blocking=True)
+        ctx.set_trace_device(d_tok, d_req, tr.n_requests)
+        ctx.set_snapshots(0, snaps)
+        out["hit_sum"].zero_()
+        g.run(out=out)
+        h_hit.copy_(out["hit"], non_blocking=True)
+        g.select(out)
+        torch.cuda.synchronize()
+
+    for _ in range(2):
+        one()
+    steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = time.perf_counter() - t0
+    import torch.distributed as dist
+    if dist.is_initialized():
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t[0])
+    return {"value": n_units * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "note": "wall clock incl. H2D of trace+requests+snapshots (pinned/pageable host) and D2H of hits"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/*
+ * marconi.h -- C ABI of libmarconi.so: B200 (sm_100a) α-grid trace replay of
+ * Marconi's hybrid-model radix-tree prefix cache (arXiv 2411.19379).
+ *
+ * The method:
+ *   - hybrid "all-or-nothing" longest-prefix lookup: a hit needs the KVs of every
+ *     prefix token and one SSM state that matches the prefix exactly
+ *     (§3; §2.2);
+ *   - judicious admission by speculative insertion: checkpoint the SSM state at a
+ *     branch point found by a dry-run insertion of the input, and at the last
+ *     decoded token (§4.1, fig:spec_insertion);
+ *   - FLOP-aware eviction: utility S(n) = recency(n) + α·flop_efficiency(n)
+ *     (Eq. 2), both min-max normalised over all nodes,
+ *     flop_efficiency = FLOPs saved / bytes of all states (Eq. 1, PAPER:395-397,
+ *     Appendix A tab:flops_breakdown PAPER:771-772, conv_1d PAPER:814), the
+ *     argmin evicted until the request fits; candidates are nodes
+ *     with <= 1 child, an evicted 1-child node is absorbed by its child, a hit
+ *     touches only the accessed node (§4.3);
+ *   - α tuning: replay the bootstrap requests from a tree snapshot for a grid of
+ *     α and adopt the α with the best token hit rate (§4.2).
+ * The readings where the paper is silent are listed in DESIGN.md ("Readings").
+ *
+ * Conventions
+ *   - Every function returns an mc_status (negative = error) and never throws.
+ *     mc_last_error() returns a thread-local message for the last failure.
+ *   - d_* arguments are DEVICE pointers (CUDA global memory, e.g. torch tensors),
+ *     h_* arguments are HOST pointers.  The caller owns every buffer it passes;
+ *     device buffers passed to mc_set_trace are BORROWED for the context's
+ *     lifetime.  Snapshot stores are owned by the context (allocated by the
+ *     setup calls mc_set_snapshots / mc_live_pass, freed by mc_destroy).
+ *     Nothing is allocated on the replay path.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Compute calls are asynchronous on it; argument errors are returned
+ *     synchronously; device-side failures (node-table overflow, an invariant
+ *     such as "hit <= input length" or "capacity respected" broken) set a device
+ *     status word that mc_check() reads.
+ *   - Requests are numbered 1..n_reqs in trace order; request r's logical
+ *     timestamp is r (reading R3).
+ *   - Results never depend on the stream, the chain order, the chain subset
+ *     passed to one call, or the launch configuration.
+ */
+#ifndef MARCONI_H_
+#define MARCONI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MC_OK = 0,
+  MC_EINVAL = -1,     /* invalid argument (returned synchronously)                 */
+  MC_ENOMEM = -2,     /* device allocation failed / workspace too small            */
+  MC_ECUDA = -3,      /* CUDA runtime error                                        */
+  MC_EOVERFLOW = -4,  /* node table (max_nodes) or snapshot store overflow         */
+  MC_ESTATE = -5,     /* call order (e.g. replay before set_trace)                 */
+  MC_EDEVICE = -6     /* device status word: an invariant was violated on device   */
+} mc_status;
+
+/* ModelConfig: layer counts {Attention, SSM, MLP}, D = d_model,
+ * N = d_state, bytes per parameter (1, 2 or 4; fp16 = 2) and the
+ * conv_1d state shape. */
+typedef struct {
+  uint32_t n_attn, n_ssm, n_mlp, d_model, d_state, bytes_per_param, conv_in, conv_kernel;
+} mc_model;
+
+/* One cache configuration.  capacity_bytes = UINT64_MAX means unlimited bytes,
+ * 0 = no cache (every request bypasses admission).  capacity_nodes
+ * caps the number of non-root nodes (0 = no node cap; the toy config uses 6). */
+typedef struct {
+  mc_model model;
+  uint64_t capacity_bytes;
+  uint32_t capacity_nodes;
+  uint32_t reserved;
+} mc_variant;
+
+/* Request r (1-based, at index r-1): sequence = tokens[tok_off, tok_off + input_len
+ * + output_len), input = the first input_len tokens. */
+typedef struct {
+  uint64_t tok_off;
+  uint32_t input_len, output_len;
+} mc_request;
+
+/* Canonical snapshot record (one radix node).  id 0 is the root (never listed);
+ * parent_id 0 = child of the root.  The node's edge is tokens[ref_off + d_start,
+ * ref_off + d_end); its SSM state (if has_ssm) represents depth d_end. */
+typedef struct {
+  uint32_t id, parent_id;
+  uint64_t ref_off;
+  uint32_t d_start, d_end, t_last, has_ssm;
+} mc_snap_node;
+
+/* Replay window: requests first_req .. first_req + n_req - 1 from snapshot
+ * `snapshot` of the chain's variant (SURVEY.md §8(c) c.2 "Grid"). */
+typedef struct {
+  uint32_t first_req, n_req, snapshot, reserved;
+} mc_segment;
+
+/* One eviction: request, victim node id, kind (0 leaf removal, 1 absorption
+ * into the single child), live non-root nodes scanned, utility S (Eq. 2). */
+typedef struct {
+  uint32_t req, node_id, kind, n_live;
+  double utility;
+} mc_evict_rec;
+
+typedef struct mc_ctx mc_ctx;
+
+/* Create a context for n_variants cache variants.  max_nodes (power of two,
+ * 64 .. 2^20) sizes each chain's node table; exceeding it is MC_EOVERFLOW.
+ * Validation: bytes_per_param in {1,2,4}; n_attn >= 1 (a node without KVs and
+ * without state would be zero bytes); d_model >= 1. */
+mc_status mc_create(const mc_variant* h_variants, uint32_t n_variants, uint32_t max_nodes, int device,
+                    mc_ctx** out);
+void mc_destroy(mc_ctx* ctx);
+
+/* Borrow the trace (device pointers).  Validated synchronously (input_len >= 1,
+ * ranges inside the pool, n_reqs < 2^31). */
+mc_status mc_set_trace(mc_ctx* ctx, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
+                       uint32_t n_reqs);
+
+/* Upload n_snapshots canonical snapshots for `variant` from host memory:
+ * snapshot k is h_nodes[h_offsets[k] .. h_offsets[k+1]) with next node id
+ * h_next_id[k].  Records may be in any order; parent links are resolved on the
+ * device.  Replaces the variant's snapshot store.  Synchronous on `stream`. */
+mc_status mc_set_snapshots(mc_ctx* ctx, uint32_t variant, const mc_snap_node* h_nodes, const uint64_t* h_offsets,
+                           const uint32_t* h_next_id, uint32_t n_snapshots, void* stream);
+
+/* The α = 0 live LRU pass (α = 0 falls back to LRU) over the whole
+ * trace from an empty cache, for every variant at once, on the device.  Stores
+ * snapshot k = the tree after request k*window (k = 0 .. ceil(R/window)-1;
+ * snapshot 0 is empty) in each variant's snapshot store, and writes the live
+ * per-request outputs d_hit/d_flops/d_bypass [n_variants][n_reqs] (nullable).
+ * Needs a workspace of mc_workspace_size(ctx, n_variants) bytes. */
+mc_status mc_live_pass(mc_ctx* ctx, uint32_t window, void* d_workspace, uint64_t workspace_bytes,
+                       uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, void* stream);
+
+/* Number of snapshots held for a variant and copy one back as canonical
+ * records sorted by id (host).  *n_out receives the record count; h_out may be
+ * NULL to query it. */
+mc_status mc_snapshot_count(const mc_ctx* ctx, uint32_t variant, uint32_t* n_out);
+mc_status mc_get_snapshot(mc_ctx* ctx, uint32_t variant, uint32_t k, mc_snap_node* h_out, uint64_t cap,
+                          uint64_t* n_out, uint32_t* next_id);
+
+/* Replay windows.  Chain c = ((variant * n_alpha) + alpha_idx) * n_segs + seg. */
+mc_status mc_set_segments(mc_ctx* ctx, const mc_segment* h_segs, uint32_t n_segs);
+
+/* Workspace bytes for `n_workers` concurrent chains (one warp each; 0 = the
+ * default: every SM filled at the kernel's occupancy) and up to n_chains chain
+ * ids per mc_replay call (0 = every chain of n_alpha α values). */
+mc_status mc_workspace_size(const mc_ctx* ctx, uint32_t n_workers, uint32_t n_alpha, uint32_t n_chains,
+                            uint64_t* bytes);
+/* Worker count a workspace of `bytes` supports (the replay uses min(this, chains)). */
+mc_status mc_workspace_workers(const mc_ctx* ctx, uint64_t bytes, uint32_t n_alpha, uint32_t n_chains,
+                               uint32_t* n_workers);
+
+typedef struct {
+  const double* h_alphas;   /* [n_alpha], each >= 0 and not NaN            */
+  uint32_t n_alpha;
+  const uint32_t* h_chains; /* chain ids to run on this call (this rank's shard);     */
+  uint32_t n_chains;        /* NULL = all chains                                      */
+  void* d_workspace;
+  uint64_t workspace_bytes;
+  uint32_t* d_hit;          /* [n_variants][n_alpha][n_reqs]  hit tokens per request   */
+  uint64_t* d_flops;        /* [n_variants][n_alpha][n_reqs]  FLOPs saved = F(hit)     */
+  uint8_t* d_bypass;        /* [n_variants][n_alpha][n_reqs]  nullable                 */
+  uint64_t* d_hit_sum;      /* [n_variants][n_alpha]  += Σ hits of the chains run      */
+  uint64_t* d_counters;     /* [n_chains_total][4] nullable: Σ compared token positions,
+                               Σ visited nodes, Σ nodes scanned by evictions,
+                               Σ node records written                                 */
+  mc_evict_rec* d_log;      /* [n_chains_total][log_cap] nullable: eviction log        */
+  uint32_t log_cap;
+  uint32_t* d_log_n;        /* [n_chains_total] records produced (may exceed log_cap)  */
+  uint32_t* d_chain_ns;     /* [n_chains_total] nullable: per-chain clock64 cycles      */
+  uint32_t n_workers;       /* 0 = default (derived from the workspace size)          */
+} mc_replay_args;
+
+/* Run the chains (asynchronous on `stream`).  Each chain loads its snapshot,
+ * replays its window at its α and writes per-request outputs and its hit sum. */
+mc_status mc_replay(mc_ctx* ctx, const mc_replay_args* args, void* stream);
+
+/* Synchronise `stream` and map the device status word to an mc_status. */
+mc_status mc_check(mc_ctx* ctx, void* stream);
+
+const char* mc_last_error(void);
+
+/* ---- unit-level kernels (same device code as the replay), for parity tests ---- */
+
+/* K1 flop_byte_model, batched: per node, saved = F(d_end) - F(d_start) with
+ * F(L) = Σ_layers tab:flops_breakdown row 1 (exact u64), bytes = KVs of the edge
+ * + has_ssm * (SSM + conv states), eff = saved / bytes (IEEE fp64, Eq. 1). */
+mc_status mc_node_cost(const mc_model* h_model, uint32_t n, const uint32_t* d_d_start, const uint32_t* d_d_end,
+                       const uint8_t* d_has_ssm, uint64_t* d_saved, uint64_t* d_bytes, double* d_eff, void* stream);
+
+/* K3 score_argmin, segmented: table s is rows [d_off[s], d_off[s+1]) of
+ * (t_last, candidate, id, eff); bounds over ALL rows of the table, utility
+ * u = rec + α_s * effn (Eq. 2, degenerate range -> 0.5) for candidate rows,
+ * victim = lexicographic min (u, t_last, id).  d_best[s] = row index (or
+ * 0xFFFFFFFF if no candidate), d_u[s] = its utility. */
+mc_status mc_score_argmin(uint32_t n_tables, const uint32_t* d_off, const uint32_t* d_t, const uint8_t* d_cand,
+                          const uint32_t* d_id, const double* d_eff, const double* d_alpha, uint32_t* d_best,
+                          double* d_u, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARCONI_H_ */

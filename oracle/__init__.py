@@ -63,6 +63,7 @@ def lib():
         L.orc_prefill_flops.argtypes = [P, U64, P]
         L.orc_layer_terms.argtypes = [P, U64, P]
         L.orc_node_cost.argtypes = [P, U64, U64, U32, P, P, P]
+        L.orc_score_argmin.argtypes = [U32, P, P, P, P, D, P, P]
         L.orc_run_chains.argtypes = [P, P, P, P, P, P, P, P, P, P, P, U32, P, U64, P, P, P, U32, P,
                                      P, P, P, P, P, U32]
         _LIB = L
@@ -113,6 +114,20 @@ def node_cost(model, d_start: int, d_end: int, has_ssm: bool) -> Tuple[int, int,
     mm = _model(model)
     _check(lib().orc_node_cost(C.byref(mm), d_start, d_end, int(bool(has_ssm)), _ptr(s), _ptr(b), _ptr(e)))
     return int(s[0]), int(b[0]), float(e[0])
+
+
+def score_argmin(t, cand, ids, eff, alpha: float):
+    """Eviction choice on an explicit table (Eq. 2 + min-max normalisation + (u, t, id) argmin).
+    Returns (row index or None, utility)."""
+    t = np.ascontiguousarray(t, np.uint32)
+    cand = np.ascontiguousarray(cand, np.uint8)
+    ids = np.ascontiguousarray(ids, np.uint32)
+    eff = np.ascontiguousarray(eff, np.float64)
+    b = np.zeros(1, np.uint32)
+    u = np.zeros(1, np.float64)
+    _check(lib().orc_score_argmin(t.shape[0], _ptr(t), _ptr(cand), _ptr(ids), _ptr(eff), float(alpha),
+                                  _ptr(b), _ptr(u)))
+    return (None if b[0] == 0xFFFFFFFF else int(b[0])), float(u[0])
 
 
 # --------------------------------------------------------------------------

@@ -521,6 +521,38 @@ int orc_node_cost(const orc_model* m, u64 d_start, u64 d_end, u32 has_ssm, u64* 
           *eff = flop_efficiency(d_start, d_end, has_ssm != 0, *m))
 }
 
+// Eviction scoring on an explicit node table:
+// bounds over ALL rows, utility for candidate rows, lexicographic (u, t, id) min.
+// *best = row index or 0xFFFFFFFF when no row is a candidate.
+int orc_score_argmin(u32 n, const u32* t, const uint8_t* cand, const u32* id, const double* eff, double alpha,
+                     u32* best, double* u_out) {
+  *best = 0xFFFFFFFFu;
+  *u_out = 0;
+  if (n == 0) return 0;
+  u32 tmin = t[0], tmax = t[0];
+  double emin = eff[0], emax = eff[0];
+  for (u32 i = 0; i < n; i++) {
+    tmin = std::min(tmin, t[i]);
+    tmax = std::max(tmax, t[i]);
+    emin = std::min(emin, eff[i]);
+    emax = std::max(emax, eff[i]);
+  }
+  double bu = 0;
+  for (u32 i = 0; i < n; i++) {
+    if (!cand[i]) continue;
+    double rec = (tmax == tmin) ? 0.5 : (double)(t[i] - tmin) / (double)(tmax - tmin);
+    double effn = (emax == emin) ? 0.5 : (eff[i] - emin) / (emax - emin);
+    double u = rec + alpha * effn;
+    if (*best == 0xFFFFFFFFu || u < bu ||
+        (u == bu && (t[i] < t[*best] || (t[i] == t[*best] && id[i] < id[*best])))) {
+      *best = i;
+      bu = u;
+    }
+  }
+  *u_out = bu;
+  return 0;
+}
+
 void* orc_create(const orc_model* m, u64 cap_bytes, u32 cap_nodes, double alpha, const u32* tokens,
                  u64 n_tokens, const u64* off, const u32* lin, const u32* lout, u32 n_req) {
   try {

@@ -1,0 +1,650 @@
+// marconi.cu -- kernels and C ABI of libmarconi.so (see include/marconi.h).
+//
+// Kernels (all sm_100a, hand-written, no tensor cores -- nothing on the path is
+// a dense contraction):
+//   replay_kernel     K5: persistent; each warp pops chains (variant, α, segment)
+//                     from a device queue, loads the segment snapshot and
+//                     replays the window (K1-K4 inlined, see replay.cuh).
+//   live_kernel       the α = 0 live LRU pass per variant, dumping snapshot k
+//                     after every `window` requests (segment mode, R19).
+//   snap_link_kernel  resolves parent ids of uploaded canonical snapshots.
+//   node_cost_kernel  K1 batched (unit parity).
+//   score_argmin_kernel  K3 segmented, one warp per table (unit parity).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "marconi.h"
+#include "replay.cuh"
+
+using namespace mcd;
+
+namespace {
+thread_local std::string g_err;
+
+mc_status fail(mc_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+#define CU(x)                                                                               \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) return fail(MC_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kWarpsPerCta = 4;
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * kWarpsPerCta) replay_kernel(KParams P) {
+  const uint32_t lane = lane_id();
+  const uint32_t worker = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  if (worker >= P.n_workers) return;
+  for (;;) {
+    uint32_t qi = 0;
+    if (lane == 0) qi = atomicAdd(P.queue, 1u);
+    qi = __shfl_sync(FULL, qi, 0);
+    if (qi >= P.n_chains) return;
+    const long long t0 = clock64();
+    const uint32_t c = P.chains[qi];
+    const uint32_t s = c % P.n_segs;
+    const uint32_t a = (c / P.n_segs) % P.n_alpha;
+    const uint32_t v = c / (P.n_segs * P.n_alpha);
+    const DevVariant V = P.var[v];
+    const mc_segment seg = P.segs[s];
+    Chain C;
+    chain_init(C, P, worker, V, P.alphas[a]);
+    load_snapshot(C, P, &P.snap[v], seg.snapshot);
+    mc_evict_rec* log = P.log ? P.log + (uint64_t)c * P.log_cap : nullptr;
+    uint32_t* log_n = P.log ? P.log_n + c : nullptr;
+    if (lane == 0 && log_n) *log_n = 0;
+    unsigned long long sum = 0;
+    const uint64_t obase = ((uint64_t)v * P.n_alpha + a) * P.n_req;
+    for (uint32_t i = 0; i < seg.n_req && !C.failed; i++) {
+      const uint32_t r = seg.first_req + i;
+      const ReqOut o = process_request(C, P, r, log, log_n);
+      if (lane == 0) {
+        P.hit[obase + r - 1] = o.reuse;
+        P.flops[obase + r - 1] = o.flops;
+        if (P.bypass) P.bypass[obase + r - 1] = o.bypass ? 1 : 0;
+      }
+      sum += o.reuse;
+    }
+    if (lane == 0) {
+      atomicAdd(P.hit_sum + (uint64_t)v * P.n_alpha + a, sum);
+      if (P.counters) {
+        P.counters[4ull * c + 0] = C.c_cmp;
+        P.counters[4ull * c + 1] = C.c_vis;
+        P.counters[4ull * c + 2] = C.c_scan;
+        P.counters[4ull * c + 3] = C.c_wr;
+      }
+      if (P.chain_cycles) P.chain_cycles[c] = (uint32_t)min((long long)0xFFFFFFFF, (clock64() - t0) >> 10);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(32) live_kernel(KParams P) {
+  const uint32_t lane = lane_id();
+  const uint32_t v = blockIdx.x;
+  if (v >= P.n_var) return;
+  Chain C;
+  chain_init(C, P, v, P.var[v], 0.0);
+  load_snapshot(C, P, nullptr, 0);  // empty tree
+  DevSnapOut* out = P.live_out + v;
+  dump_snapshot(C, P, out, 0);
+  for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
+    const ReqOut o = process_request(C, P, r, nullptr, nullptr);
+    if (lane == 0) {
+      const uint64_t k = (uint64_t)v * P.n_req + r - 1;
+      if (P.hit) P.hit[k] = o.reuse;
+      if (P.flops) P.flops[k] = o.flops;
+      if (P.bypass) P.bypass[k] = o.bypass ? 1 : 0;
+    }
+    if (r % P.window == 0 && r < P.n_req) dump_snapshot(C, P, out, r / P.window);
+  }
+}
+
+// parent_idx of uploaded canonical records (sorted by id within each snapshot).
+__global__ void snap_link_kernel(const mc_snap_node* nodes, const uint64_t* off, uint32_t n_snap, uint32_t* pidx,
+                                 uint32_t* status) {
+  const uint32_t k = blockIdx.y;
+  if (k >= n_snap) return;
+  const uint64_t a = off[k], b = off[k + 1];
+  const uint32_t n = (uint32_t)(b - a);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t pid = nodes[a + i].parent_id;
+    uint32_t res = NIL;
+    if (pid != 0) {
+      uint32_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (nodes[a + mid].id < pid) lo = mid + 1; else hi = mid;
+      }
+      if (lo < n && nodes[a + lo].id == pid) res = lo;
+      else atomicOr(status, ST_INVARIANT);
+    }
+    pidx[a + i] = res;
+  }
+}
+
+__global__ void node_cost_kernel(DevModel m, uint32_t n, const uint32_t* ds, const uint32_t* de, const uint8_t* ssm,
+                                 unsigned long long* saved, unsigned long long* bytes, double* eff) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t a = ds[i], b = de[i];
+    const bool s = ssm[i] != 0;
+    saved[i] = prefill_F(m, b) - prefill_F(m, a);
+    bytes[i] = node_bytes(m, a, b, s);
+    eff[i] = node_eff(m, a, b, s);
+  }
+}
+
+__global__ void score_argmin_kernel(uint32_t n_tables, const uint32_t* off, const uint32_t* t, const uint8_t* cand,
+                                    const uint32_t* id, const double* eff, const double* alpha, uint32_t* best_out,
+                                    double* u_out) {
+  const uint32_t lane = lane_id();
+  const uint32_t s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= n_tables) return;
+  const uint32_t a = off[s], b = off[s + 1];
+  Bounds bd;
+  bounds_init(bd);
+  for (uint32_t i = a + lane; i < b; i += 32) bounds_add(bd, t[i], eff[i]);
+  bounds_reduce(bd);
+  Best best;
+  best_init(best);
+  const double al = alpha[s];
+  for (uint32_t i = a + lane; i < b; i += 32) {
+    if (!cand[i]) continue;
+    const double u = utility(bd, t[i], eff[i], al);
+    if (best.i == NIL || better(u, t[i], id[i], best)) {
+      best.u = u; best.t = t[i]; best.id = id[i]; best.i = i - a;
+    }
+  }
+  best_reduce(best);
+  if (lane == 0) {
+    best_out[s] = best.i;
+    u_out[s] = best.i == NIL ? 0.0 : best.u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+struct SnapStore {
+  mc_snap_node* nodes = nullptr;
+  uint32_t* pidx = nullptr;
+  uint64_t* off = nullptr;
+  uint32_t* n = nullptr;
+  uint32_t* nid = nullptr;
+  uint32_t count = 0;
+  uint64_t cap = 0;
+  void release() {
+    cudaFree(nodes); cudaFree(pidx); cudaFree(off); cudaFree(n); cudaFree(nid);
+    *this = SnapStore();
+  }
+};
+
+struct mc_ctx {
+  int device = 0;
+  int n_sm = 0;
+  int blocks_per_sm = 1;
+  uint32_t ncap = 0, hcap = 0;
+  std::vector<mc_variant> hv;
+  std::vector<DevVariant> dvh;
+  DevVariant* d_var = nullptr;
+  const uint32_t* tok = nullptr;
+  uint64_t n_tok = 0;
+  const mc_request* req = nullptr;
+  uint32_t n_req = 0;
+  std::vector<SnapStore> snaps;
+  DevSnapStore* d_stores = nullptr;
+  std::vector<mc_segment> segs;
+  mc_segment* d_segs = nullptr;
+  uint32_t* d_status = nullptr;
+  double* d_alphas = nullptr;  // small device buffer (64 entries)
+  uint32_t alpha_cap = 0;
+};
+
+namespace {
+constexpr uint64_t kCtrl = 4096;  // workspace control header (queue counter, ...)
+
+DevModel make_model(const mc_model& m) {
+  // Appendix A tab:flops_breakdown summed over layers, and PAPER:814.
+  const unsigned __int128 D = m.d_model, N = m.d_state;
+  unsigned __int128 fa = 8 * (unsigned __int128)m.n_attn * D * D +
+                         (unsigned __int128)m.n_ssm * (12 * D * D + 16 * D * N + 10) +
+                         16 * (unsigned __int128)m.n_mlp * D * D;
+  unsigned __int128 fb = 4 * (unsigned __int128)m.n_attn * D;
+  DevModel d;
+  d.fa = (uint64_t)fa;
+  d.fb = (uint64_t)fb;
+  d.kvt = (uint64_t)m.n_attn * 2ull * m.d_model * m.bytes_per_param;
+  d.ssmb = (uint64_t)m.n_ssm *
+           ((uint64_t)m.d_model * m.d_state + (uint64_t)m.conv_in * m.conv_kernel) * m.bytes_per_param;
+  d.n_ssm = m.n_ssm;
+  d.pad = 0;
+  return d;
+}
+
+mc_status upload_stores(mc_ctx* c) {
+  std::vector<DevSnapStore> h(c->snaps.size());
+  for (size_t v = 0; v < c->snaps.size(); v++) {
+    h[v].nodes = c->snaps[v].nodes;
+    h[v].pidx = c->snaps[v].pidx;
+    h[v].off = c->snaps[v].off;
+    h[v].n = c->snaps[v].n;
+    h[v].nid = c->snaps[v].nid;
+    h[v].count = c->snaps[v].count;
+    h[v].pad = 0;
+  }
+  CU(cudaMemcpy(c->d_stores, h.data(), sizeof(DevSnapStore) * h.size(), cudaMemcpyHostToDevice));
+  return MC_OK;
+}
+
+uint32_t default_workers(const mc_ctx* c) { return (uint32_t)(c->n_sm * c->blocks_per_sm * kWarpsPerCta); }
+}  // namespace
+
+extern "C" {
+
+const char* mc_last_error(void) { return g_err.c_str(); }
+
+mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, int device, mc_ctx** out) {
+  if (!out || !hv || n_var == 0) return fail(MC_EINVAL, "mc_create: null argument or no variants");
+  *out = nullptr;
+  if (max_nodes < 64 || max_nodes > (1u << 20) || (max_nodes & (max_nodes - 1)))
+    return fail(MC_EINVAL, "max_nodes must be a power of two in [64, 2^20]");
+  for (uint32_t v = 0; v < n_var; v++) {
+    const mc_model& m = hv[v].model;
+    if (m.bytes_per_param != 1 && m.bytes_per_param != 2 && m.bytes_per_param != 4)
+      return fail(MC_EINVAL, "bytes_per_param must be 1, 2 or 4 (SPEC:36)");
+    if (m.n_attn == 0) return fail(MC_EINVAL, "n_attn = 0 would allow zero-byte nodes (SPEC:136)");
+    if (m.d_model == 0) return fail(MC_EINVAL, "d_model must be >= 1");
+    // F(L) must stay exact in fp64 (< 2^53) for L up to 2^20 tokens handled below per trace
+  }
+  CU(cudaSetDevice(device));
+  mc_ctx* c = new mc_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    delete c;
+    return fail(MC_ECUDA, "cudaGetDeviceProperties failed");
+  }
+  c->n_sm = prop.multiProcessorCount;
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel, 32 * kWarpsPerCta, 0);
+  c->blocks_per_sm = std::max(1, bps);
+  c->ncap = max_nodes;
+  c->hcap = 2 * max_nodes;
+  c->hv.assign(hv, hv + n_var);
+  for (uint32_t v = 0; v < n_var; v++) {
+    DevVariant d;
+    d.m = make_model(hv[v].model);
+    d.cap_bytes = hv[v].capacity_bytes;
+    d.cap_nodes = hv[v].capacity_nodes;
+    d.pad = 0;
+    c->dvh.push_back(d);
+  }
+  c->snaps.resize(n_var);
+  c->alpha_cap = 256;
+  if (cudaMalloc(&c->d_var, sizeof(DevVariant) * n_var) != cudaSuccess ||
+      cudaMalloc(&c->d_stores, sizeof(DevSnapStore) * n_var) != cudaSuccess ||
+      cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&c->d_alphas, sizeof(double) * c->alpha_cap) != cudaSuccess) {
+    mc_destroy(c);
+    return fail(MC_ENOMEM, "mc_create: device allocation failed");
+  }
+  cudaMemcpy(c->d_var, c->dvh.data(), sizeof(DevVariant) * n_var, cudaMemcpyHostToDevice);
+  cudaMemset(c->d_status, 0, sizeof(uint32_t));
+  if (upload_stores(c) != MC_OK) {
+    mc_destroy(c);
+    return MC_ECUDA;
+  }
+  *out = c;
+  return MC_OK;
+}
+
+void mc_destroy(mc_ctx* c) {
+  if (!c) return;
+  for (auto& s : c->snaps) s.release();
+  cudaFree(c->d_var);
+  cudaFree(c->d_stores);
+  cudaFree(c->d_segs);
+  cudaFree(c->d_status);
+  cudaFree(c->d_alphas);
+  delete c;
+}
+
+mc_status mc_set_trace(mc_ctx* c, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
+                       uint32_t n_reqs) {
+  if (!c || !d_tokens || !d_reqs || n_reqs == 0) return fail(MC_EINVAL, "mc_set_trace: null/empty argument");
+  if (n_reqs >= (1u << 31)) return fail(MC_EINVAL, "too many requests (timestamps must stay < 2^31)");
+  std::vector<mc_request> h(n_reqs);
+  CU(cudaMemcpy(h.data(), d_reqs, sizeof(mc_request) * n_reqs, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < n_reqs; i++) {
+    const mc_request& q = h[i];
+    if (q.input_len == 0) return fail(MC_EINVAL, "request " + std::to_string(i + 1) + ": input_len == 0");
+    const uint64_t n = (uint64_t)q.input_len + q.output_len;
+    if (n > (1u << 20)) return fail(MC_EINVAL, "request longer than 2^20 tokens");
+    if (q.tok_off + n > n_tokens) return fail(MC_EINVAL, "request " + std::to_string(i + 1) + ": range outside pool");
+  }
+  for (const auto& d : c->dvh) {  // F(L) exact in u64 and < 2^53 (exact fp64 conversion) for the longest request
+    uint64_t Lmax = 0;
+    for (const auto& q : h) Lmax = std::max<uint64_t>(Lmax, (uint64_t)q.input_len + q.output_len);
+    unsigned __int128 F = (unsigned __int128)d.m.fa * Lmax + (unsigned __int128)d.m.fb * Lmax * Lmax;
+    if (F >= ((unsigned __int128)1 << 53)) return fail(MC_EINVAL, "F(L) exceeds 2^53 for the longest request");
+  }
+  c->tok = d_tokens;
+  c->n_tok = n_tokens;
+  c->req = d_reqs;
+  c->n_req = n_reqs;
+  return MC_OK;
+}
+
+mc_status mc_set_snapshots(mc_ctx* c, uint32_t variant, const mc_snap_node* h_nodes, const uint64_t* h_off,
+                           const uint32_t* h_nid, uint32_t n_snap, void* stream) {
+  if (!c || variant >= c->hv.size() || !h_off || !h_nid || n_snap == 0)
+    return fail(MC_EINVAL, "mc_set_snapshots: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_set_snapshots before mc_set_trace");
+  const uint64_t total = h_off[n_snap];
+  if (h_off[0] != 0) return fail(MC_EINVAL, "h_offsets[0] must be 0");
+  // Records must be sorted by id within each snapshot for the device-side parent
+  // resolution; sort a copy only when the caller's order is not already sorted.
+  bool is_sorted = true;
+  for (uint32_t k = 0; k < n_snap; k++) {
+    if (h_off[k + 1] < h_off[k]) return fail(MC_EINVAL, "offsets must be non-decreasing");
+    if (h_off[k + 1] - h_off[k] + 1 > c->ncap) return fail(MC_EOVERFLOW, "snapshot larger than max_nodes");
+    for (uint64_t i = h_off[k] + 1; i < h_off[k + 1]; i++)
+      if (h_nodes[i - 1].id >= h_nodes[i].id) is_sorted = false;
+  }
+  std::vector<mc_snap_node> sorted;
+  const mc_snap_node* src = h_nodes;
+  if (!is_sorted) {
+    sorted.assign(h_nodes, h_nodes + total);
+    for (uint32_t k = 0; k < n_snap; k++)
+      std::sort(sorted.begin() + h_off[k], sorted.begin() + h_off[k + 1],
+                [](const mc_snap_node& a, const mc_snap_node& b) { return a.id < b.id; });
+    src = sorted.data();
+  }
+  for (uint32_t k = 0; k < n_snap; k++) {
+    for (uint64_t i = h_off[k]; i < h_off[k + 1]; i++) {
+      const mc_snap_node& r = src[i];
+      if (r.id == 0 || (i > h_off[k] && src[i - 1].id == r.id)) return fail(MC_EINVAL, "bad/duplicate node id");
+      if (r.d_end <= r.d_start || r.ref_off + r.d_end > c->n_tok) return fail(MC_EINVAL, "bad node range");
+    }
+  }
+  SnapStore& s = c->snaps[variant];
+  const uint64_t nn = std::max<uint64_t>(total, 1);
+  if (s.cap < nn || s.count < n_snap || !s.nodes) {  // reuse the store when it is large enough
+    s.release();
+    if (cudaMalloc(&s.nodes, sizeof(mc_snap_node) * nn) != cudaSuccess ||
+        cudaMalloc(&s.pidx, sizeof(uint32_t) * nn) != cudaSuccess ||
+        cudaMalloc(&s.off, sizeof(uint64_t) * (n_snap + 1)) != cudaSuccess ||
+        cudaMalloc(&s.n, sizeof(uint32_t) * n_snap) != cudaSuccess ||
+        cudaMalloc(&s.nid, sizeof(uint32_t) * n_snap) != cudaSuccess) {
+      s.release();
+      return fail(MC_ENOMEM, "snapshot store allocation failed");
+    }
+    s.cap = nn;
+  }
+  std::vector<uint32_t> cnt(n_snap);
+  for (uint32_t k = 0; k < n_snap; k++) cnt[k] = (uint32_t)(h_off[k + 1] - h_off[k]);
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(s.nodes, src, sizeof(mc_snap_node) * total, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(s.off, h_off, sizeof(uint64_t) * (n_snap + 1), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(s.n, cnt.data(), sizeof(uint32_t) * n_snap, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(s.nid, h_nid, sizeof(uint32_t) * n_snap, cudaMemcpyHostToDevice, st));
+  dim3 grid(8, n_snap);
+  snap_link_kernel<<<grid, 256, 0, st>>>(s.nodes, s.off, n_snap, s.pidx, c->d_status);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(st));
+  s.count = n_snap;
+  return upload_stores(c);
+}
+
+mc_status mc_workspace_size(const mc_ctx* c, uint32_t n_workers, uint32_t n_alpha, uint32_t n_chains,
+                            uint64_t* bytes) {
+  if (!c || !bytes) return fail(MC_EINVAL, "mc_workspace_size: null argument");
+  if (n_workers == 0) n_workers = default_workers(c);
+  if (n_chains == 0) n_chains = (uint32_t)(c->hv.size() * std::max(1u, n_alpha) * std::max<size_t>(1, c->segs.size()));
+  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
+  *bytes = head + (uint64_t)n_workers * ws_bytes_per_worker(c->ncap, c->hcap);
+  return MC_OK;
+}
+
+mc_status mc_workspace_workers(const mc_ctx* c, uint64_t bytes, uint32_t n_alpha, uint32_t n_chains,
+                               uint32_t* n_workers) {
+  if (!c || !n_workers) return fail(MC_EINVAL, "mc_workspace_workers: null argument");
+  if (n_chains == 0) n_chains = (uint32_t)(c->hv.size() * std::max(1u, n_alpha) * std::max<size_t>(1, c->segs.size()));
+  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
+  *n_workers = bytes <= head ? 0 : (uint32_t)((bytes - head) / ws_bytes_per_worker(c->ncap, c->hcap));
+  return MC_OK;
+}
+
+mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,
+                       uint64_t* d_flops, uint8_t* d_bypass, void* stream) {
+  if (!c || !d_ws || window == 0) return fail(MC_EINVAL, "mc_live_pass: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
+  const uint32_t nv = (uint32_t)c->hv.size();
+  const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
+  if (ws_bytes < kCtrl + per * nv) return fail(MC_ENOMEM, "workspace too small for the live pass");
+  const uint32_t K = (c->n_req + window - 1) / window;
+  std::vector<DevSnapOut> outs(nv);
+  for (uint32_t v = 0; v < nv; v++) {
+    SnapStore& s = c->snaps[v];
+    s.release();
+    const uint64_t cap = (uint64_t)K * c->ncap;
+    if (cudaMalloc(&s.nodes, sizeof(mc_snap_node) * cap) != cudaSuccess ||
+        cudaMalloc(&s.pidx, sizeof(uint32_t) * cap) != cudaSuccess ||
+        cudaMalloc(&s.off, sizeof(uint64_t) * (K + 1)) != cudaSuccess ||
+        cudaMalloc(&s.n, sizeof(uint32_t) * K) != cudaSuccess ||
+        cudaMalloc(&s.nid, sizeof(uint32_t) * K) != cudaSuccess) {
+      s.release();
+      return fail(MC_ENOMEM, "snapshot store allocation failed");
+    }
+    s.count = K;
+    s.cap = cap;
+    outs[v].nodes = s.nodes;
+    outs[v].pidx = s.pidx;
+    outs[v].off = s.off;
+    outs[v].n = s.n;
+    outs[v].nid = s.nid;
+    outs[v].stride = c->ncap;
+    outs[v].count = K;
+    outs[v].pad = 0;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  DevSnapOut* d_outs = (DevSnapOut*)((char*)d_ws + 256);
+  if (sizeof(DevSnapOut) * nv + 256 > kCtrl) return fail(MC_EINVAL, "too many variants for the live pass");
+  CU(cudaMemcpyAsync(d_outs, outs.data(), sizeof(DevSnapOut) * nv, cudaMemcpyHostToDevice, st));
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.tok = c->tok;
+  P.n_tok = c->n_tok;
+  P.req = c->req;
+  P.n_req = c->n_req;
+  P.n_var = nv;
+  P.var = c->d_var;
+  P.ncap = c->ncap;
+  P.hcap = c->hcap;
+  P.n_workers = nv;
+  P.ws = (char*)d_ws + kCtrl;
+  P.ws_stride = per;
+  P.hit = d_hit;
+  P.flops = (unsigned long long*)d_flops;
+  P.bypass = d_bypass;
+  P.status = c->d_status;
+  P.live_out = d_outs;
+  P.window = window;
+  live_kernel<<<nv, 32, 0, st>>>(P);
+  CU(cudaGetLastError());
+  // the last snapshot offset entry (K) for completeness
+  std::vector<uint64_t> offK(1, (uint64_t)K * c->ncap);
+  for (uint32_t v = 0; v < nv; v++)
+    CU(cudaMemcpyAsync(c->snaps[v].off + K, offK.data(), sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  return upload_stores(c);
+}
+
+mc_status mc_snapshot_count(const mc_ctx* c, uint32_t variant, uint32_t* n_out) {
+  if (!c || !n_out || variant >= c->hv.size()) return fail(MC_EINVAL, "mc_snapshot_count: bad argument");
+  *n_out = c->snaps[variant].count;
+  return MC_OK;
+}
+
+mc_status mc_get_snapshot(mc_ctx* c, uint32_t variant, uint32_t k, mc_snap_node* h_out, uint64_t cap,
+                          uint64_t* n_out, uint32_t* next_id) {
+  if (!c || !n_out || variant >= c->hv.size()) return fail(MC_EINVAL, "mc_get_snapshot: bad argument");
+  const SnapStore& s = c->snaps[variant];
+  if (k >= s.count) return fail(MC_EINVAL, "snapshot index out of range");
+  CU(cudaDeviceSynchronize());
+  uint64_t off = 0;
+  uint32_t n = 0, nid = 0;
+  CU(cudaMemcpy(&off, s.off + k, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&n, s.n + k, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&nid, s.nid + k, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  *n_out = n;
+  if (next_id) *next_id = nid;
+  if (!h_out) return MC_OK;
+  if (cap < n) return fail(MC_EINVAL, "output buffer too small");
+  CU(cudaMemcpy(h_out, s.nodes + off, sizeof(mc_snap_node) * n, cudaMemcpyDeviceToHost));
+  std::sort(h_out, h_out + n, [](const mc_snap_node& a, const mc_snap_node& b) { return a.id < b.id; });
+  return MC_OK;
+}
+
+mc_status mc_set_segments(mc_ctx* c, const mc_segment* h_segs, uint32_t n_segs) {
+  if (!c || !h_segs || n_segs == 0) return fail(MC_EINVAL, "mc_set_segments: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_set_segments before mc_set_trace");
+  for (uint32_t i = 0; i < n_segs; i++) {
+    const mc_segment& s = h_segs[i];
+    if (s.first_req < 1 || (uint64_t)s.first_req + s.n_req - 1 > c->n_req)
+      return fail(MC_EINVAL, "segment " + std::to_string(i) + " outside the trace");
+  }
+  cudaFree(c->d_segs);
+  c->d_segs = nullptr;
+  CU(cudaMalloc(&c->d_segs, sizeof(mc_segment) * n_segs));
+  CU(cudaMemcpy(c->d_segs, h_segs, sizeof(mc_segment) * n_segs, cudaMemcpyHostToDevice));
+  c->segs.assign(h_segs, h_segs + n_segs);
+  return MC_OK;
+}
+
+mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
+  if (!c || !A) return fail(MC_EINVAL, "mc_replay: null argument");
+  if (!c->tok || c->segs.empty()) return fail(MC_ESTATE, "mc_replay before mc_set_trace/mc_set_segments");
+  if (!A->h_alphas || A->n_alpha == 0 || A->n_alpha > c->alpha_cap) return fail(MC_EINVAL, "bad alpha grid");
+  for (uint32_t i = 0; i < A->n_alpha; i++)
+    if (!(A->h_alphas[i] >= 0.0) || A->h_alphas[i] == __builtin_inf())
+      return fail(MC_EINVAL, "alpha must be finite and >= 0 (SPEC:308)");
+  if (!A->d_workspace || !A->d_hit || !A->d_flops || !A->d_hit_sum) return fail(MC_EINVAL, "null output buffer");
+  const uint32_t nv = (uint32_t)c->hv.size(), ns = (uint32_t)c->segs.size();
+  const uint64_t total_chains = (uint64_t)nv * A->n_alpha * ns;
+  if (total_chains >= (1ull << 32)) return fail(MC_EINVAL, "too many chains");
+  for (uint32_t v = 0; v < nv; v++)
+    for (const auto& s : c->segs)
+      if (s.snapshot >= c->snaps[v].count)
+        return fail(MC_ESTATE, "segment snapshot index missing for variant " + std::to_string(v));
+  const uint32_t n_chains = A->h_chains ? A->n_chains : (uint32_t)total_chains;
+  if (n_chains == 0) return MC_OK;
+  std::vector<uint32_t> ids;
+  if (A->h_chains) {
+    for (uint32_t i = 0; i < n_chains; i++)
+      if (A->h_chains[i] >= total_chains) return fail(MC_EINVAL, "chain id out of range");
+  } else {
+    ids.resize(n_chains);
+    for (uint32_t i = 0; i < n_chains; i++) ids[i] = i;
+  }
+  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
+  const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
+  if (A->workspace_bytes < head + per) return fail(MC_ENOMEM, "workspace too small");
+  uint32_t workers = (uint32_t)((A->workspace_bytes - head) / per);
+  if (A->n_workers) workers = std::min(workers, A->n_workers);
+  workers = std::min(workers, n_chains);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)A->d_workspace;
+  CU(cudaMemsetAsync(ws, 0, 256, st));
+  CU(cudaMemcpyAsync(ws + kCtrl, A->h_chains ? A->h_chains : ids.data(), 4ull * n_chains, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(c->d_alphas, A->h_alphas, sizeof(double) * A->n_alpha, cudaMemcpyHostToDevice, st));
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.tok = c->tok;
+  P.n_tok = c->n_tok;
+  P.req = c->req;
+  P.n_req = c->n_req;
+  P.n_var = nv;
+  P.var = c->d_var;
+  P.snap = c->d_stores;
+  P.segs = c->d_segs;
+  P.n_segs = ns;
+  P.n_alpha = A->n_alpha;
+  P.alphas = c->d_alphas;
+  P.chains = (const uint32_t*)(ws + kCtrl);
+  P.n_chains = n_chains;
+  P.ncap = c->ncap;
+  P.hcap = c->hcap;
+  P.n_workers = workers;
+  P.queue = (unsigned*)ws;
+  P.ws = ws + head;
+  P.ws_stride = per;
+  P.hit = A->d_hit;
+  P.flops = (unsigned long long*)A->d_flops;
+  P.bypass = A->d_bypass;
+  P.hit_sum = (unsigned long long*)A->d_hit_sum;
+  P.counters = (unsigned long long*)A->d_counters;
+  P.log = A->d_log;
+  P.log_cap = A->log_cap;
+  P.log_n = A->d_log_n;
+  P.chain_cycles = A->d_chain_ns;
+  P.status = c->d_status;
+  const uint32_t ctas = (workers + kWarpsPerCta - 1) / kWarpsPerCta;
+  replay_kernel<<<ctas, 32 * kWarpsPerCta, 0, st>>>(P);
+  CU(cudaGetLastError());
+  return MC_OK;
+}
+
+mc_status mc_check(mc_ctx* c, void* stream) {
+  if (!c) return fail(MC_EINVAL, "mc_check: null context");
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  uint32_t st = 0;
+  CU(cudaMemcpy(&st, c->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (st) {
+    cudaMemset(c->d_status, 0, sizeof(uint32_t));
+    std::string m = "device status:";
+    if (st & ST_OVERFLOW) m += " node-table overflow (raise max_nodes);";
+    if (st & ST_INVARIANT) m += " invariant violated (capacity / hit <= input / snapshot);";
+    if (st & ST_NOCAND) m += " no eviction candidate;";
+    if (st & ST_SNAPOVF) m += " snapshot store overflow;";
+    return fail((st & (ST_OVERFLOW | ST_SNAPOVF)) ? MC_EOVERFLOW : MC_EDEVICE, m);
+  }
+  return MC_OK;
+}
+
+mc_status mc_node_cost(const mc_model* m, uint32_t n, const uint32_t* ds, const uint32_t* de, const uint8_t* ssm,
+                       uint64_t* saved, uint64_t* bytes, double* eff, void* stream) {
+  if (!m || (n && (!ds || !de || !ssm || !saved || !bytes || !eff))) return fail(MC_EINVAL, "mc_node_cost: null");
+  if (n == 0) return MC_OK;
+  const int blocks = (int)std::min<uint32_t>((n + 255) / 256, 148 * 8);
+  node_cost_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(make_model(*m), n, ds, de, ssm,
+                                                             (unsigned long long*)saved, (unsigned long long*)bytes,
+                                                             eff);
+  CU(cudaGetLastError());
+  return MC_OK;
+}
+
+mc_status mc_score_argmin(uint32_t n_tables, const uint32_t* off, const uint32_t* t, const uint8_t* cand,
+                          const uint32_t* id, const double* eff, const double* alpha, uint32_t* best, double* u,
+                          void* stream) {
+  if (n_tables == 0) return MC_OK;
+  if (!off || !t || !cand || !id || !eff || !alpha || !best || !u) return fail(MC_EINVAL, "mc_score_argmin: null");
+  const int wpb = 4;
+  score_argmin_kernel<<<(n_tables + wpb - 1) / wpb, 32 * wpb, 0, (cudaStream_t)stream>>>(n_tables, off, t, cand, id,
+                                                                                         eff, alpha, best, u);
+  CU(cudaGetLastError());
+  return MC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+"""α-grid driver (K6): chain sharding, replay, NCCL all-gather of per-α hit sums, α*.
+
+The paper tunes α by replaying the bootstrap requests from a tree snapshot for
+every α in a grid, "parallelized across CPU cores", and adopts the α that
+maximises the hit rate (§4.2 "Managing the balance").  Here the
+unit of work is a chain (variant, α, segment) replayed by one warp; chains are
+sharded across the GPUs of one box (one process per GPU), each GPU reduces its
+chains' hits into u64[n_variant, n_alpha], one all_gather_into_tensor over
+NCCL (NVLink/NVSwitch) exchanges them, and every rank takes the same argmax
+(ties -> smallest α).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import marconi as M
+
+
+def chain_id(v: int, a: int, s: int, n_alpha: int, n_segs: int) -> int:
+    return (v * n_alpha + a) * n_segs + s
+
+
+def chain_costs(lens: np.ndarray, segs, n_var: int, n_alpha: int) -> np.ndarray:
+    """Estimated cost per chain id: tokens of the window + a per-request constant."""
+    cs = np.cumsum(np.r_[0, lens.astype(np.int64)])
+    seg_cost = np.asarray([cs[f - 1 + n] - cs[f - 1] + 256 * n for f, n, _ in segs], np.int64)
+    return np.tile(seg_cost, n_var * n_alpha)
+
+
+def lpt_shard(costs: np.ndarray, n_segs: int, n_alpha: int, world: int) -> List[np.ndarray]:
+    """Deterministic longest-processing-time assignment of chains to ranks.
+
+    Chains are taken by decreasing cost (ties: variant, segment, α -- so the α
+    siblings of a segment stay adjacent and share trace tokens in L2) and each
+    goes to the least-loaded rank (ties: lowest rank).  Every rank computes the
+    same assignment.  Returns, per rank, its chain ids in execution order.
+    """
+    ids = np.arange(costs.shape[0], dtype=np.int64)
+    s = ids % n_segs
+    a = (ids // n_segs) % n_alpha
+    v = ids // (n_segs * n_alpha)
+    order = np.lexsort((a, s, v, -costs))
+    load = np.zeros(world, np.int64)
+    out = [[] for _ in range(world)]
+    for c in order:
+        r = int(np.argmin(load))
+        out[r].append(int(c))
+        load[r] += int(costs[c])
+    return [np.asarray(x, np.uint32) for x in out]
+
+
+def select_alpha(alphas: Sequence[float], hit_sums: np.ndarray) -> List[float]:
+    """Per variant: α* = argmax Σ hits (equal denominators Σ L_in), ties -> smallest α."""
+    alphas = np.asarray(alphas, np.float64)
+    order = np.argsort(alphas, kind="stable")
+    res = []
+    for row in np.asarray(hit_sums).reshape(-1, len(alphas)):
+        best = None
+        for i in order:
+            if best is None or row[i] > row[best]:
+                best = i
+        res.append(float(alphas[best]))
+    return res
+
+
+class AlphaGrid:
+    """One rank's share of an α-grid replay over segment windows.
+
+    setup(): trace -> device, α = 0 live pass on the device producing the
+    segment snapshots S_k (tree after request k*W), segments, this rank's chain
+    shard and the workspace.  run(): replay the shard (async).  select():
+    all-gather the per-α hit sums and return α* per variant.
+    """
+
+    def __init__(self, trace, variants, alphas: Sequence[float], n_segments: int, rank: int = 0, world: int = 1,
+                 max_nodes: int = 8192, device: int = 0, group=None):
+        self.trace = trace
+        self.variants = list(variants)
+        self.alphas = [float(a) for a in alphas]
+        self.n_segments = n_segments
+        self.rank, self.world = rank, world
+        self.group = group
+        self.ctx = M.Context(self.variants, max_nodes=max_nodes, device=device)
+        R = trace.n_requests
+        self.window = -(-R // n_segments)
+        self.segs = []
+        for k in range(n_segments):
+            a, b = k * self.window, min((k + 1) * self.window, R)
+            if b > a:
+                self.segs.append((a + 1, b - a, k))
+
+    def setup(self, snapshots=None):
+        """snapshots: optional {variant: [(nodes, next_id), ...]} to upload instead of the device live pass."""
+        tr = self.trace
+        self.d_tokens, self.d_reqs = self.ctx.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
+        if snapshots is None:
+            self.live = self.ctx.live_pass(self.window)
+        else:
+            for v, snaps in snapshots.items():
+                self.ctx.set_snapshots(v, snaps)
+            self.live = None
+        self.ctx.set_segments(self.segs)
+        lens = tr.lin.astype(np.int64) + tr.lout
+        costs = chain_costs(lens, self.segs, len(self.variants), len(self.alphas))
+        self.shards = lpt_shard(costs, len(self.segs), len(self.alphas), self.world)
+        self.chains = self.shards[self.rank]
+        self.workspace = self.ctx.alloc_workspace(0, len(self.alphas), len(self.chains))
+        return self
+
+    @property
+    def n_chains_total(self) -> int:
+        return len(self.variants) * len(self.alphas) * len(self.segs)
+
+    def run(self, out=None, **kw):
+        return self.ctx.replay(self.alphas, chains=self.chains, workspace=self.workspace, out=out, **kw)
+
+    def select(self, out) -> List[float]:
+        import torch
+        hs = out["hit_sum"]
+        if self.world > 1:
+            import torch.distributed as dist
+            g = torch.empty((self.world,) + tuple(hs.shape), dtype=hs.dtype, device=hs.device)
+            dist.all_gather_into_tensor(g, hs.contiguous(), group=self.group)
+            hs = g.sum(0)
+        self.hit_sums = hs.cpu().numpy()
+        return select_alpha(self.alphas, self.hit_sums)

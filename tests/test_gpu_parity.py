@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (north_star): bit-exact hit tokens, FLOPs saved, bypass flags, eviction
+order (request, node id, kind) and chosen α; utilities compared by bit pattern
+(the contractual bound is 1e-12 relative, checked as well).
+"""
+import numpy as np
+import pytest
+
+import gpu_util as GU
+import oracle as O
+import scenarios as SC
+import tracegen as tg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2411_19379_b200 import marconi as M  # noqa: E402
+from paper_2411_19379_b200 import AlphaGrid  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _assert_logs_equal(glog, gn, olog, ctx=""):
+    assert gn == len(olog), (ctx, gn, len(olog))
+    assert np.array_equal(glog["req"], olog["req"]), ctx
+    assert np.array_equal(glog["node_id"], olog["node_id"]), ctx
+    assert np.array_equal(glog["kind"], olog["kind"]), ctx
+    assert np.array_equal(glog["n_live"], olog["n_live"]), ctx
+    gu, ou = glog["utility"], olog["utility"]
+    assert np.all(np.abs(gu - ou) <= 1e-12 * np.maximum(1.0, np.abs(ou))), ctx
+    assert np.array_equal(gu.view(np.uint64), ou.view(np.uint64)), ctx  # bitwise
+
+
+# ---------------------------------------------------------------- K1
+def test_k1_node_cost_bitexact():
+    rng = np.random.default_rng(1)
+    models = [tg.MODEL_7B, tg.MODEL_TOY, tg.model_ratio(2), tg.model_ratio(4), tg.model_ratio(8),
+              tg.Model(4, 0, 4), tg.Model(4, 24, 28, d_state=16), tg.Model(4, 24, 28, bytes_per_param=4)]
+    n = 3000
+    for m in models:
+        ds = rng.integers(0, 32768, n).astype(np.int32)
+        ln = rng.integers(1, 32768, n)
+        ln[:50] = 1
+        de = np.minimum(ds + ln, 65535).astype(np.int32)
+        ssm = (rng.random(n) < 0.6).astype(np.uint8)
+        if m.n_ssm == 0:
+            ssm[:] = 0
+        s, b, e = M.node_cost(m, torch.from_numpy(ds).to(DEV), torch.from_numpy(de).to(DEV),
+                              torch.from_numpy(ssm).to(DEV))
+        s, b, e = s.cpu().numpy(), b.cpu().numpy(), e.cpu().numpy()
+        for i in range(0, n, 7):
+            os_, ob, oe = O.node_cost(m, int(ds[i]), int(de[i]), bool(ssm[i]))
+            assert int(s[i]) == os_ and int(b[i]) == ob
+            assert np.float64(e[i]).view(np.uint64) == np.float64(oe).view(np.uint64)
+
+
+# ---------------------------------------------------------------- K3
+def test_k3_score_argmin_segmented():
+    rng = np.random.default_rng(2)
+    tabs = []
+    for k in range(600):
+        n = int(rng.integers(0, 3000)) if k % 50 == 0 else int(rng.integers(1, 200))
+        t = rng.integers(1, 5000, n).astype(np.uint32)
+        if k % 3 == 0 and n:
+            t[:] = t[0]                                 # degenerate recency range
+        eff = rng.uniform(1e3, 3e5, n)
+        if k % 5 == 0 and n > 3:
+            eff[1:4] = eff[0]                           # equal eff -> ties on u
+            t[1:4] = t[0]                               # ... and on t: id decides
+        cand = (rng.random(n) < 0.6).astype(np.uint8)
+        ids = (rng.permutation(n) + 1).astype(np.uint32)
+        a = float(tg.ALPHA_GRID16[k % 16])
+        tabs.append((t, cand, ids, eff, a))
+    off = np.zeros(len(tabs) + 1, np.int32)
+    off[1:] = np.cumsum([len(x[0]) for x in tabs])
+    cat = lambda i, dt: torch.from_numpy(np.concatenate([x[i] for x in tabs]).astype(dt)).to(DEV)
+    best, u = M.score_argmin(torch.from_numpy(off).to(DEV), cat(0, np.int32), cat(1, np.uint8), cat(2, np.int32),
+                             cat(3, np.float64), torch.tensor([x[4] for x in tabs], dtype=torch.float64, device=DEV))
+    best, u = best.cpu().numpy(), u.cpu().numpy()
+    for k, (t, cand, ids, eff, a) in enumerate(tabs):
+        ob, ou = O.score_argmin(t, cand, ids, eff, a)
+        if ob is None:
+            assert best[k] == -1
+        else:
+            assert best[k] == ob, k
+            assert np.float64(u[k]).view(np.uint64) == np.float64(ou).view(np.uint64)
+
+
+# ---------------------------------------------------------------- scenarios
+SPEC = SC.load()
+
+
+@pytest.mark.parametrize("sc", SPEC["scenarios"], ids=lambda s: s["name"])
+def test_scenarios_on_gpu(sc):
+    tr = SC.scenario_trace(SPEC, sc)
+    v = SC.variant(sc)
+    g, out = GU.gpu_grid(tr, [v], sc["alphas"], 1, max_nodes=64, log_cap=64)
+    hit = out["hit"].cpu().numpy()
+    for ai, a in enumerate(sc["alphas"]):
+        assert hit[0, ai].tolist() == sc["hits"], (a, hit[0, ai])
+        h, f, b, lg = GU.oracle_chain_log(tr, v, a, 1, tr.n_requests, (np.zeros(0, O.NODE_DTYPE), 1))
+        assert np.array_equal(out["flops"].cpu().numpy()[0, ai], f.astype(np.int64))
+        glog, gn = g.ctx.read_log(out, ai)
+        _assert_logs_equal(glog, gn, lg, sc["name"])
+
+
+@pytest.mark.parametrize("ex", SPEC["eviction_examples"], ids=lambda s: s["name"])
+def test_eviction_examples_on_gpu(ex):
+    tr, nodes, nid = SC.eviction_example(SPEC, ex)
+    snap = np.zeros(len(nodes), M.SNAP_DTYPE)
+    for i, (a, b, c, d, e, f, g) in enumerate(nodes):
+        snap[i] = (a, b, c, d, e, f, g)
+    alphas = [float(a) for a in ex["expect"]]
+    ctx = M.Context([tg.Variant(SC.MODELS[ex["model"]], tg.UNLIMITED_BYTES, ex["cap_nodes"])], max_nodes=64)
+    ctx.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
+    ctx.set_snapshots(0, [(snap, nid)])
+    ctx.set_segments([(ex["request"], 1, 0)])
+    out = ctx.replay(alphas, log_cap=8)
+    ctx.check()
+    for ai, a in enumerate(alphas):
+        glog, gn = ctx.read_log(out, ai)
+        want = ex["expect"][str(a) if str(a) in ex["expect"] else repr(a)]
+        assert (int(glog[0]["node_id"]), int(glog[0]["kind"])) == (want["node_id"], want["kind"])
+        _, _, _, lg = GU.oracle_chain_log(tr, ctx.variants[0], a, ex["request"], 1,
+                                          (snap.astype(O.NODE_DTYPE), nid))
+        _assert_logs_equal(glog, gn, lg, ex["name"])
+
+
+# ---------------------------------------------------------------- micro traces
+def _micro_variant(seed):
+    k = seed % 3
+    ssmb = 26_787_840
+    kvt = 65_536
+    if k == 0:
+        return tg.Variant(tg.MODEL_7B, tg.UNLIMITED_BYTES, 2 + seed % 6)
+    if k == 1:
+        return tg.Variant(tg.MODEL_7B, (2 + seed % 4) * ssmb + (seed % 50) * kvt, 0)
+    return tg.Variant(tg.MODEL_7B, (3 + seed % 3) * ssmb, 3 + seed % 5)
+
+
+def test_micro_traces_full_parity():
+    """300 micro traces: live-pass snapshots, every chain's hits/flops/bypass and eviction log."""
+    for seed in range(300):
+        tr = tg.micro_trace(seed, n_req=20, max_len=64, alphabet=2 + seed % 3)
+        v = _micro_variant(seed)
+        alphas = [0.0, tg.ALPHA_GRID16[seed % 16], 64.0]
+        g, out = GU.gpu_grid(tr, [v], alphas, 2, max_nodes=128, log_cap=256)
+        snaps, live, res, segs = GU.oracle_grid(tr, [v], alphas, 2, threads=1)
+        # device live pass == oracle live pass (per request and snapshots)
+        lh, lf, lb = (x.cpu().numpy()[0] for x in g.live)
+        assert np.array_equal(lh, live[0][0]) and np.array_equal(lf, live[0][1].astype(np.int64)), seed
+        assert np.array_equal(lb, live[0][2].astype(np.uint8)), seed
+        for k in range(len(snaps[0])):
+            gs, gn = g.ctx.get_snapshot(0, k)
+            on, onid = snaps[0][k]
+            assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), (seed, k)
+        hit, fl, by = (out[x].cpu().numpy() for x in ("hit", "flops", "bypass"))
+        for cid, (h, f, b, ctr) in res.items():
+            ai, si = cid // len(segs), cid % len(segs)
+            first, n, k = segs[si]
+            sl = slice(first - 1, first - 1 + n)
+            assert np.array_equal(hit[0, ai, sl], h), (seed, cid)
+            assert np.array_equal(fl[0, ai, sl], f.astype(np.int64)), (seed, cid)
+            assert np.array_equal(by[0, ai, sl], b.astype(np.uint8)), (seed, cid)
+            _, _, _, lg = GU.oracle_chain_log(tr, v, alphas[ai], first, n, snaps[0][k])
+            glog, gn = g.ctx.read_log(out, cid)
+            _assert_logs_equal(glog, gn, lg, f"seed {seed} chain {cid}")
+
+
+def test_toy_config_and_family():
+    """Config 1 (toy: 16 requests, {4,28,32}, 6-node cache, α in {0,1}) plus 200 seeds of its family."""
+    for seed in [1001] + list(range(5000, 5200)):
+        w = tg.workload(1) if seed == 1001 else None
+        tr = w.trace if w else tg.toy_trace(seed, 16)
+        var = tg.Variant(tg.MODEL_TOY, tg.UNLIMITED_BYTES, 6)
+        g, out = GU.gpu_grid(tr, [var], (0.0, 1.0), 1, max_nodes=64, log_cap=64)
+        a_star = g.select(out)
+        sums = []
+        for ai, a in enumerate((0.0, 1.0)):
+            h, f, b, lg = GU.oracle_chain_log(tr, var, a, 1, tr.n_requests, (np.zeros(0, O.NODE_DTYPE), 1))
+            assert np.array_equal(out["hit"].cpu().numpy()[0, ai], h), seed
+            glog, gn = g.ctx.read_log(out, ai)
+            _assert_logs_equal(glog, gn, lg, f"toy {seed}")
+            sums.append(int(h.sum()))
+        assert a_star[0] == O.select_alpha((0.0, 1.0), sums)
+
+
+def _compare_grid(w, R_cap_nodes=8192, log_cap=0, threads=0):
+    tr = w.trace
+    g, out = GU.gpu_grid(tr, w.variants, w.alphas, w.n_segments, max_nodes=R_cap_nodes, log_cap=log_cap,
+                         counters=True)
+    snaps, live, res, segs = GU.oracle_grid(tr, w.variants, w.alphas, w.n_segments, threads=threads)
+    hit, fl, by = (out[x].cpu().numpy() for x in ("hit", "flops", "bypass"))
+    ctr = out["counters"].cpu().numpy()
+    na, ns = len(w.alphas), len(segs)
+    for v in range(len(w.variants)):
+        for k in range(len(snaps[v])):
+            gs, gn = g.ctx.get_snapshot(v, k)
+            on, onid = snaps[v][k]
+            assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), (v, k)
+    for cid, (h, f, b, c) in res.items():
+        v, ai, si = cid // (na * ns), (cid // ns) % na, cid % ns
+        first, n, k = segs[si]
+        sl = slice(first - 1, first - 1 + n)
+        assert np.array_equal(hit[v, ai, sl], h), cid
+        assert np.array_equal(fl[v, ai, sl], f.astype(np.int64)), cid
+        assert np.array_equal(by[v, ai, sl], b.astype(np.uint8)), cid
+        assert np.array_equal(ctr[cid], c.astype(np.int64)), (cid, ctr[cid], c)
+        if log_cap:
+            _, _, _, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[v][k])
+            glog, gn = g.ctx.read_log(out, cid)
+            _assert_logs_equal(glog, gn, lg, f"chain {cid}")
+    # α* per variant
+    a_star = g.select(out)
+    for v in range(len(w.variants)):
+        sums = [sum(int(res[(v * na + ai) * ns + si][0].sum()) for si in range(ns)) for ai in range(na)]
+        assert a_star[v] == O.select_alpha(w.alphas, sums)
+    return g, out
+
+
+def test_config3_reduced_full_parity():
+    w = tg.workload(3, R=4000)
+    w.n_segments = 8
+    _compare_grid(w, log_cap=4096)
+
+
+def test_config2_reduced():
+    w = tg.workload(2, R=2500)
+    _compare_grid(w, log_cap=8192)
+
+
+def test_config4_reduced():
+    w = tg.workload(4, R=800)
+    w.alphas = (0.0, 1 / 16, 1.0, 64.0)
+    w.n_segments = 4
+    _compare_grid(w, log_cap=2048)
+
+
+def test_config5_reduced():
+    w = tg.workload(5, R=3000)
+    w.alphas = (0.0, 1.0)
+    w.n_segments = 2
+    _compare_grid(w)
+
+
+def test_uploaded_snapshots_match_live_pass():
+    """mc_set_snapshots with the ORACLE's snapshots gives the same results as the device live pass."""
+    w = tg.workload(3, R=3000)
+    alphas = (0.0, 0.5, 4.0)
+    snaps, live, res, segs = GU.oracle_grid(w.trace, w.variants, alphas, 6)
+    g, out = GU.gpu_grid(w.trace, w.variants, alphas, 6, snapshots={0: snaps[0]})
+    hit = out["hit"].cpu().numpy()
+    for cid, (h, f, b, c) in res.items():
+        ai, si = cid // len(segs), cid % len(segs)
+        first, n, k = segs[si]
+        assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h)
+
+
+def test_chain_subsets_and_order_do_not_matter():
+    w = tg.workload(3, R=3000)
+    alphas = tg.ALPHA_GRID16[::3]
+    g, out = GU.gpu_grid(w.trace, w.variants, alphas, 6)
+    total = g.n_chains_total
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(total).astype(np.uint32)
+    halves = [perm[: total // 2], perm[total // 2:]]
+    o2 = g.ctx.alloc_outputs(len(alphas))
+    for h in halves:
+        g.ctx.replay(alphas, chains=h, out=o2, n_workers=7)
+    g.ctx.check()
+    for key in ("hit", "flops", "bypass", "hit_sum"):
+        assert torch.equal(out[key], o2[key]), key
+
+
+def test_full_config3_sampled():
+    """BASELINE.json configs[2] at full size (50k requests, 16 α x 128 segments, the bench launch):
+    device snapshots and sampled chains vs the oracle; invariants on every chain."""
+    w = tg.workload(3)
+    tr = w.trace
+    g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
+    out = g.run(counters=True)
+    g.ctx.check()
+    hit = out["hit"].cpu().numpy()
+    # invariants at full size: hit <= L_in; α = 0 segment replay == device live pass
+    assert (hit <= tr.lin[None, None, :]).all()
+    lh = g.live[0].cpu().numpy()[0]
+    assert np.array_equal(hit[0, 0], lh)
+    # sampled snapshots / chains against the oracle
+    W = g.window
+    sample_k = [1, 37, 127]
+    snaps, h_live, f_live, b_live = O.live_pass(tr, w.variants[0], W, upto=max(sample_k) * W)
+    assert np.array_equal(lh[: len(h_live)], h_live)
+    for k in sample_k:
+        gs, gn = g.ctx.get_snapshot(0, k)
+        on, onid = snaps[k]
+        assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), k
+    ns = len(g.segs)
+    for k in sample_k:
+        for ai in (0, 5, 8, 15):
+            first, n, _ = g.segs[k]
+            h, f, b, lg = GU.oracle_chain_log(tr, w.variants[0], w.alphas[ai], first, n, snaps[k])
+            assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h), (k, ai)
+    a_star = g.select(out)
+    assert a_star[0] in w.alphas
+
+
+def test_errors_are_loud():
+    tr = tg.workload(3, R=2000).trace
+    v = tg.Variant(tg.MODEL_7B, 60 * tg.GB)
+    ctx = M.Context([v], max_nodes=64)   # far too small for this trace
+    ctx.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
+    with pytest.raises(M.MarconiError) as e:
+        ctx.live_pass(200)
+    assert "MC_EOVERFLOW" in str(e.value)
+    ctx2 = M.Context([v], max_nodes=8192)
+    ctx2.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
+    ctx2.live_pass(1000)
+    ctx2.set_segments([(1, 1000, 0)])
+    with pytest.raises(M.MarconiError):
+        ctx2.replay([-1.0])
+    with pytest.raises(M.MarconiError):
+        M.Context([tg.Variant(tg.Model(0, 4, 4), 10)], max_nodes=64)
