@@ -36,13 +36,16 @@ mc_status fail(mc_status s, const std::string& m) {
     if (e_ != cudaSuccess) return fail(MC_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+#ifndef MC_MINBLOCKS
+#define MC_MINBLOCKS 4
+#endif
 constexpr int kWarpsPerCta = 4;
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(32 * kWarpsPerCta) replay_kernel(KParams P) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel(KParams P) {
   const uint32_t lane = lane_id();
   const uint32_t worker = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (worker >= P.n_workers) return;

@@ -109,14 +109,8 @@ struct KParams {
   uint32_t window;
 };
 
-// Per-worker workspace slice (SoA node table + dense live list + hash).
-struct WS {
-  uint32_t *id, *parent, *ds, *de, *t, *nchild, *cxor, *ftok, *flags, *dpos, *dslot, *path, *freel, *hval;
-  unsigned long long* hkey;
-  uint64_t* roff;
-  DenseRec* dense;
-};
-
+// Per-worker workspace slice (SoA node table + dense live list + hash).  Only the
+// base pointer and sizes live in registers; array addresses are recomputed.
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
   uint64_t b = 14ull * 4 * ncap  // 13 u32 node arrays (+1 spare)
                + 8ull * ncap     // roff
@@ -125,26 +119,34 @@ __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t 
   return (b + 255) & ~255ull;
 }
 
+struct WS {
+  char* b;
+  uint32_t n, h;
+  __device__ __forceinline__ DenseRec* dense() const { return (DenseRec*)b; }
+  __device__ __forceinline__ uint64_t* roff() const { return (uint64_t*)(b + 16ull * n); }
+  __device__ __forceinline__ unsigned long long* hkey() const { return (unsigned long long*)(b + 24ull * n); }
+  __device__ __forceinline__ uint32_t* a32(uint32_t k) const { return (uint32_t*)(b + 24ull * n + 8ull * h + 4ull * k * n); }
+  __device__ __forceinline__ uint32_t* id() const { return a32(0); }
+  __device__ __forceinline__ uint32_t* parent() const { return a32(1); }
+  __device__ __forceinline__ uint32_t* ds() const { return a32(2); }
+  __device__ __forceinline__ uint32_t* de() const { return a32(3); }
+  __device__ __forceinline__ uint32_t* t() const { return a32(4); }
+  __device__ __forceinline__ uint32_t* nchild() const { return a32(5); }
+  __device__ __forceinline__ uint32_t* cxor() const { return a32(6); }
+  __device__ __forceinline__ uint32_t* ftok() const { return a32(7); }
+  __device__ __forceinline__ uint32_t* flags() const { return a32(8); }
+  __device__ __forceinline__ uint32_t* dpos() const { return a32(9); }
+  __device__ __forceinline__ uint32_t* dslot() const { return a32(10); }
+  __device__ __forceinline__ uint32_t* path() const { return a32(11); }
+  __device__ __forceinline__ uint32_t* freel() const { return a32(12); }
+  __device__ __forceinline__ uint32_t* hval() const { return (uint32_t*)(b + 24ull * n + 8ull * h + 52ull * n); }
+};
+
 __device__ inline WS ws_slice(char* base, uint32_t ncap, uint32_t hcap) {
   WS w;
-  char* p = base;
-  w.dense = (DenseRec*)p; p += 16ull * ncap;
-  w.roff = (uint64_t*)p; p += 8ull * ncap;
-  w.hkey = (unsigned long long*)p; p += 8ull * hcap;
-  w.id = (uint32_t*)p; p += 4ull * ncap;
-  w.parent = (uint32_t*)p; p += 4ull * ncap;
-  w.ds = (uint32_t*)p; p += 4ull * ncap;
-  w.de = (uint32_t*)p; p += 4ull * ncap;
-  w.t = (uint32_t*)p; p += 4ull * ncap;
-  w.nchild = (uint32_t*)p; p += 4ull * ncap;
-  w.cxor = (uint32_t*)p; p += 4ull * ncap;
-  w.ftok = (uint32_t*)p; p += 4ull * ncap;
-  w.flags = (uint32_t*)p; p += 4ull * ncap;
-  w.dpos = (uint32_t*)p; p += 4ull * ncap;
-  w.dslot = (uint32_t*)p; p += 4ull * ncap;
-  w.path = (uint32_t*)p; p += 4ull * ncap;
-  w.freel = (uint32_t*)p; p += 4ull * ncap;
-  w.hval = (uint32_t*)p; p += 4ull * hcap;
+  w.b = base;
+  w.n = ncap;
+  w.h = hcap;
   return w;
 }
 
@@ -271,12 +273,12 @@ __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t pare
   const uint32_t lane = lane_id();
   for (uint32_t base = 0; base <= C.hmask; base += 32) {
     const uint32_t idx = (h + base + lane) & C.hmask;
-    const unsigned long long k = C.w.hkey[idx];
+    const unsigned long long k = C.w.hkey()[idx];
     const unsigned mm = __ballot_sync(FULL, k == key);
     const unsigned me = __ballot_sync(FULL, k == EMPTY);
     if (mm) {
       const int fm = __ffs(mm) - 1;
-      if (!me || fm < __ffs(me) - 1) return C.w.hval[(h + base + fm) & C.hmask];
+      if (!me || fm < __ffs(me) - 1) return C.w.hval()[(h + base + fm) & C.hmask];
       return NIL;
     }
     if (me) return NIL;
@@ -288,7 +290,7 @@ __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t pare
 __device__ __forceinline__ uint32_t hash_index_1(const Chain& C, unsigned long long key) {
   uint32_t i = hslot(key, C.hmask);
   for (;;) {
-    unsigned long long k = C.w.hkey[i];
+    unsigned long long k = C.w.hkey()[i];
     if (k == key) return i;
     if (k == EMPTY) return NIL;
     i = (i + 1) & C.hmask;
@@ -296,58 +298,58 @@ __device__ __forceinline__ uint32_t hash_index_1(const Chain& C, unsigned long l
 }
 __device__ __forceinline__ void hash_insert_1(Chain& C, unsigned long long key, uint32_t val) {
   uint32_t i = hslot(key, C.hmask);
-  while (C.w.hkey[i] != EMPTY) i = (i + 1) & C.hmask;
-  C.w.hkey[i] = key;
-  C.w.hval[i] = val;
+  while (C.w.hkey()[i] != EMPTY) i = (i + 1) & C.hmask;
+  C.w.hkey()[i] = key;
+  C.w.hval()[i] = val;
 }
 __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & C.hmask;
-    unsigned long long k = C.w.hkey[j];
+    unsigned long long k = C.w.hkey()[j];
     if (k == EMPTY) break;
     uint32_t home = hslot(k, C.hmask);
     bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
     if (!stays) {
-      C.w.hkey[i] = k;
-      C.w.hval[i] = C.w.hval[j];
+      C.w.hkey()[i] = k;
+      C.w.hval()[i] = C.w.hval()[j];
       i = j;
     }
   }
-  C.w.hkey[i] = EMPTY;
+  C.w.hkey()[i] = EMPTY;
 }
 
 // ---- dense live list (lane 0) ----
 __device__ __forceinline__ void dense_refresh_1(Chain& C, uint32_t s) {
-  const bool cand = C.w.nchild[s] <= 1 && !(C.w.flags[s] & F_PIN);
-  C.w.dense[C.w.dpos[s]].tc = C.w.t[s] | (cand ? 0u : NOTC);
+  const bool cand = C.w.nchild()[s] <= 1 && !(C.w.flags()[s] & F_PIN);
+  C.w.dense()[C.w.dpos()[s]].tc = C.w.t()[s] | (cand ? 0u : NOTC);
 }
 __device__ __forceinline__ void dense_set_eff_1(Chain& C, uint32_t s) {
-  C.w.dense[C.w.dpos[s]].eff = node_eff(C.m, C.w.ds[s], C.w.de[s], C.w.flags[s] & F_SSM);
+  C.w.dense()[C.w.dpos()[s]].eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
 }
 __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s) {
   const uint32_t i = C.count++;
-  C.w.dpos[s] = i;
-  C.w.dslot[i] = s;
+  C.w.dpos()[s] = i;
+  C.w.dslot()[i] = s;
   DenseRec d;
   d.tc = 0;
-  d.id = C.w.id[s];
-  d.eff = node_eff(C.m, C.w.ds[s], C.w.de[s], C.w.flags[s] & F_SSM);
-  C.w.dense[i] = d;
+  d.id = C.w.id()[s];
+  d.eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
+  C.w.dense()[i] = d;
   dense_refresh_1(C, s);
 }
 __device__ __forceinline__ void dense_remove_1(Chain& C, uint32_t s) {
-  const uint32_t i = C.w.dpos[s];
+  const uint32_t i = C.w.dpos()[s];
   const uint32_t last = --C.count;
   if (i != last) {
-    C.w.dense[i] = C.w.dense[last];
-    const uint32_t s2 = C.w.dslot[last];
-    C.w.dslot[i] = s2;
-    C.w.dpos[s2] = i;
+    C.w.dense()[i] = C.w.dense()[last];
+    const uint32_t s2 = C.w.dslot()[last];
+    C.w.dslot()[i] = s2;
+    C.w.dpos()[s2] = i;
   }
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
-  if (C.nfree) return C.w.freel[--C.nfree];
+  if (C.nfree) return C.w.freel()[--C.nfree];
   if (C.hwm >= C.ncap) {
     atomicOr(status, ST_OVERFLOW);
     C.failed = true;
@@ -375,14 +377,14 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     C.failed = true;
     return;
   }
-  for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.hkey[i] = EMPTY;
+  for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.hkey()[i] = EMPTY;
   for (uint32_t i = lane; i <= n; i += 32) {
-    C.w.nchild[i] = 0;
-    C.w.cxor[i] = 0;
+    C.w.nchild()[i] = 0;
+    C.w.cxor()[i] = 0;
   }
   if (lane == 0) {
-    C.w.id[0] = 0; C.w.parent[0] = NIL; C.w.ds[0] = 0; C.w.de[0] = 0; C.w.t[0] = 0;
-    C.w.flags[0] = 0; C.w.roff[0] = 0; C.w.ftok[0] = 0;
+    C.w.id()[0] = 0; C.w.parent()[0] = NIL; C.w.ds()[0] = 0; C.w.de()[0] = 0; C.w.t()[0] = 0;
+    C.w.flags()[0] = 0; C.w.roff()[0] = 0; C.w.ftok()[0] = 0;
   }
   __syncwarp();
   uint64_t bytes = 0;
@@ -393,33 +395,33 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     const uint32_t pi = pidx[i];
     const uint32_t ps = (pi == NIL) ? 0u : pi + 1;
     bad |= (r.d_end <= r.d_start) || (r.ref_off + r.d_end > P.n_tok) || (pi != NIL && pi >= n);
-    C.w.id[s] = r.id;
-    C.w.parent[s] = ps;
-    C.w.ds[s] = r.d_start;
-    C.w.de[s] = r.d_end;
-    C.w.t[s] = r.t_last;
-    C.w.roff[s] = r.ref_off;
-    C.w.flags[s] = r.has_ssm ? F_SSM : 0u;
+    C.w.id()[s] = r.id;
+    C.w.parent()[s] = ps;
+    C.w.ds()[s] = r.d_start;
+    C.w.de()[s] = r.d_end;
+    C.w.t()[s] = r.t_last;
+    C.w.roff()[s] = r.ref_off;
+    C.w.flags()[s] = r.has_ssm ? F_SSM : 0u;
     const uint32_t ft = P.tok[r.ref_off + r.d_start];
-    C.w.ftok[s] = ft;
-    C.w.dpos[s] = i;
-    C.w.dslot[i] = s;
-    atomicAdd(&C.w.nchild[ps], 1u);
-    atomicXor(&C.w.cxor[ps], s);
+    C.w.ftok()[s] = ft;
+    C.w.dpos()[s] = i;
+    C.w.dslot()[i] = s;
+    atomicAdd(&C.w.nchild()[ps], 1u);
+    atomicXor(&C.w.cxor()[ps], s);
     const unsigned long long key = hkey_of(ps, ft);
     uint32_t j = hslot(key, C.hmask);
-    while (atomicCAS(&C.w.hkey[j], EMPTY, key) != EMPTY) j = (j + 1) & C.hmask;
-    C.w.hval[j] = s;
+    while (atomicCAS(&C.w.hkey()[j], EMPTY, key) != EMPTY) j = (j + 1) & C.hmask;
+    C.w.hval()[j] = s;
     bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     DenseRec d;
-    d.tc = C.w.t[s] | (C.w.nchild[s] <= 1 ? 0u : NOTC);
-    d.id = C.w.id[s];
-    d.eff = node_eff(C.m, C.w.ds[s], C.w.de[s], C.w.flags[s] & F_SSM);
-    C.w.dense[i] = d;
+    d.tc = C.w.t()[s] | (C.w.nchild()[s] <= 1 ? 0u : NOTC);
+    d.id = C.w.id()[s];
+    d.eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
+    C.w.dense()[i] = d;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(FULL, (unsigned long long)bytes, o);
@@ -446,18 +448,18 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
   mc_snap_node* dst = out->nodes + (uint64_t)k * out->stride;
   uint32_t* pdst = out->pidx + (uint64_t)k * out->stride;
   for (uint32_t i = lane; i < C.count; i += 32) {
-    const uint32_t s = C.w.dslot[i];
-    const uint32_t p = C.w.parent[s];
+    const uint32_t s = C.w.dslot()[i];
+    const uint32_t p = C.w.parent()[s];
     mc_snap_node r;
-    r.id = C.w.id[s];
-    r.parent_id = (p == 0) ? 0u : C.w.id[p];
-    r.ref_off = C.w.roff[s];
-    r.d_start = C.w.ds[s];
-    r.d_end = C.w.de[s];
-    r.t_last = C.w.t[s];
-    r.has_ssm = (C.w.flags[s] & F_SSM) ? 1u : 0u;
+    r.id = C.w.id()[s];
+    r.parent_id = (p == 0) ? 0u : C.w.id()[p];
+    r.ref_off = C.w.roff()[s];
+    r.d_start = C.w.ds()[s];
+    r.d_end = C.w.de()[s];
+    r.t_last = C.w.t()[s];
+    r.has_ssm = (C.w.flags()[s] & F_SSM) ? 1u : 0u;
     dst[i] = r;
-    pdst[i] = (p == 0) ? NIL : C.w.dpos[p];
+    pdst[i] = (p == 0) ? NIL : C.w.dpos()[p];
   }
   if (lane == 0) {
     out->off[k] = (uint64_t)k * out->stride;
@@ -491,20 +493,122 @@ __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, 
 // ---------------------------------------------------------------------------
 // K3 + K4: one eviction
 // ---------------------------------------------------------------------------
-__device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
+// Exact victim selection over the dense live list (Eq. 2).
+//   α = 0: u = rec exactly and rec is strictly monotone in t, so the victim is
+//          the candidate with the smallest (t_last, id) -- one pass (LRU,
+//          PAPER:424); only the victim's u is computed.
+//   α > 0: filter and verify.  Pass 1: bounds.  Pass 2: a division-free
+//          approximate key k' = (t - tmin) * RN(1/Δt) + (e - emin) * RN(α/Δe)
+//          with |k' - u| <= 10 (1+α) 2^-53; each lane keeps its best two keys.
+//          Only entries with k' <= min k' + δ, δ = (1+α) 2^-45, can be the exact
+//          argmin; their exact u (the IEEE recipe) decides.  If any lane has
+//          two entries within δ (near-ties), fall back to the exact full pass.
+#ifndef MC_UNROLL
+#define MC_UNROLL 2
+#endif
+constexpr int kUnroll = MC_UNROLL;
+
+__device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b) {
   const uint32_t lane = lane_id();
-  const uint32_t cnt = C.count;
-  Bounds b;
-  bounds_init(b);
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const DenseRec d = C.w.dense[i];
-    bounds_add(b, d.tc & ~NOTC, d.eff);
-  }
-  bounds_reduce(b);
+  const DenseRec* __restrict__ dn = C.w.dense();
   Best best;
   best_init(best);
+  bounds_init(b);
+  if (C.alpha == 0.0) {
+    for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+      DenseRec d[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; q++) {
+        const uint32_t i = base + 32 * q + lane;
+        if (i < cnt) d[q] = dn[i];
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; q++) {
+        const uint32_t i = base + 32 * q + lane;
+        if (i >= cnt) continue;
+        const uint32_t t = d[q].tc & ~NOTC;
+        b.tmin = min(b.tmin, t);
+        b.tmax = max(b.tmax, t);
+        if (!(d[q].tc & NOTC) && (t < best.t || (t == best.t && d[q].id < best.id))) {
+          best.t = t; best.id = d[q].id; best.i = i;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      b.tmin = min(b.tmin, __shfl_xor_sync(FULL, b.tmin, o));
+      b.tmax = max(b.tmax, __shfl_xor_sync(FULL, b.tmax, o));
+      const uint32_t t = __shfl_xor_sync(FULL, best.t, o);
+      const uint32_t id = __shfl_xor_sync(FULL, best.id, o);
+      const uint32_t i = __shfl_xor_sync(FULL, best.i, o);
+      if (i != NIL && (best.i == NIL || t < best.t || (t == best.t && id < best.id))) {
+        best.t = t; best.id = id; best.i = i;
+      }
+    }
+    if (best.i != NIL) {
+      const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
+      best.u = __dadd_rn(rec, __dmul_rn(0.0, 0.5));  // = rec (α·effn = +0)
+    }
+    return best;
+  }
+  // pass 1: bounds over ALL non-root nodes (R1)
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+    DenseRec d[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < cnt) d[q] = dn[i];
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++)
+      if (base + 32 * q + lane < cnt) bounds_add(b, d[q].tc & ~NOTC, d[q].eff);
+  }
+  bounds_reduce(b);
+  // pass 2: approximate keys, best two per lane
+  const bool dt0 = b.tmax == b.tmin, de0 = b.emax == b.emin;
+  const double idt = dt0 ? 0.0 : __drcp_rn((double)(b.tmax - b.tmin));
+  const double aide = de0 ? 0.0 : __ddiv_rn(C.alpha, __dsub_rn(b.emax, b.emin));
+  const double kconst = __dadd_rn(dt0 ? 0.5 : 0.0, de0 ? __dmul_rn(C.alpha, 0.5) : 0.0);
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  double k1 = INF, k2 = INF;
+  uint32_t i1 = NIL;
+  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
+    DenseRec d[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < cnt) d[q] = dn[i];
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i >= cnt || (d[q].tc & NOTC)) continue;
+      const double k = __dadd_rn(__dadd_rn(__dmul_rn((double)(d[q].tc - b.tmin), idt),
+                                           __dmul_rn(__dsub_rn(d[q].eff, b.emin), aide)), kconst);
+      if (k < k1) { k2 = k1; k1 = k; i1 = i; }
+      else if (k < k2) { k2 = k; }
+    }
+  }
+  double kmin = k1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) kmin = fmin(kmin, __shfl_xor_sync(FULL, kmin, o));
+  if (kmin == INF) return best;  // no candidate
+  const double delta = __dmul_rn(__dadd_rn(1.0, C.alpha), 2.842170943040401e-14);  // (1+α) 2^-45
+  const double lim = __dadd_rn(kmin, delta);
+  if (!__any_sync(FULL, k2 <= lim)) {
+    if (k1 <= lim) {
+      const DenseRec d = dn[i1];
+      best.u = utility(b, d.tc, d.eff, C.alpha);
+      best.t = d.tc;
+      best.id = d.id;
+      best.i = i1;
+    }
+    best_reduce(best);
+    return best;
+  }
+  // near-ties: exact full pass
   for (uint32_t i = lane; i < cnt; i += 32) {
-    const DenseRec d = C.w.dense[i];
+    const DenseRec d = dn[i];
     if (d.tc & NOTC) continue;
     const double u = utility(b, d.tc, d.eff, C.alpha);
     if (best.i == NIL || better(u, d.tc, d.id, best)) {
@@ -512,6 +616,14 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     }
   }
   best_reduce(best);
+  return best;
+}
+
+__device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
+  const uint32_t lane = lane_id();
+  const uint32_t cnt = C.count;
+  Bounds b;
+  const Best best = select_victim(C, cnt, b);
   C.c_scan += cnt;
   if (best.i == NIL) {
     if (lane == 0) atomicOr(P.status, ST_NOCAND);
@@ -519,28 +631,28 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     return;
   }
   if (lane == 0) {
-    const uint32_t x = C.w.dslot[best.i];
-    const uint32_t p = C.w.parent[x];
-    const uint32_t xf = C.w.flags[x];
+    const uint32_t x = C.w.dslot()[best.i];
+    const uint32_t p = C.w.parent()[x];
+    const uint32_t xf = C.w.flags()[x];
     uint32_t kind;
-    if (C.w.nchild[x] == 0) {  // leaf: free KVs + state
+    if (C.w.nchild()[x] == 0) {  // leaf: free KVs + state
       kind = 0;
-      C.total -= node_bytes(C.m, C.w.ds[x], C.w.de[x], xf & F_SSM);
-      hash_erase_at_1(C, hash_index_1(C, hkey_of(p, C.w.ftok[x])));
-      C.w.nchild[p] -= 1;
-      C.w.cxor[p] ^= x;
+      C.total -= node_bytes(C.m, C.w.ds()[x], C.w.de()[x], xf & F_SSM);
+      hash_erase_at_1(C, hash_index_1(C, hkey_of(p, C.w.ftok()[x])));
+      C.w.nchild()[p] -= 1;
+      C.w.cxor()[p] ^= x;
       if (p != 0) dense_refresh_1(C, p);
       C.c_wr += 1;
     } else {  // one child: release the state, the child absorbs the KVs
       kind = 1;
-      const uint32_t c = C.w.cxor[x];
+      const uint32_t c = C.w.cxor()[x];
       if (xf & F_SSM) C.total -= C.m.ssmb;
-      hash_erase_at_1(C, hash_index_1(C, hkey_of(x, C.w.ftok[c])));
-      C.w.hval[hash_index_1(C, hkey_of(p, C.w.ftok[x]))] = c;
-      C.w.ds[c] = C.w.ds[x];
-      C.w.ftok[c] = C.w.ftok[x];
-      C.w.parent[c] = p;
-      C.w.cxor[p] ^= x ^ c;
+      hash_erase_at_1(C, hash_index_1(C, hkey_of(x, C.w.ftok()[c])));
+      C.w.hval()[hash_index_1(C, hkey_of(p, C.w.ftok()[x]))] = c;
+      C.w.ds()[c] = C.w.ds()[x];
+      C.w.ftok()[c] = C.w.ftok()[x];
+      C.w.parent()[c] = p;
+      C.w.cxor()[p] ^= x ^ c;
       dense_set_eff_1(C, c);
       C.c_wr += 2;
     }
@@ -554,8 +666,8 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       *log_n = li + 1;
     }
     dense_remove_1(C, x);
-    C.w.flags[x] = 0;
-    C.w.freel[C.nfree++] = x;
+    C.w.flags()[x] = 0;
+    C.w.freel()[C.nfree++] = x;
   }
   sync_state(C);
 }
@@ -566,25 +678,25 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
                                             uint32_t r) {
   const uint32_t u = alloc_1(C, P.status);
   if (u == NIL) return NIL;
-  const uint32_t p = C.w.parent[y];
-  const uint32_t ods = C.w.ds[y];
-  C.w.id[u] = C.next_id++;
-  C.w.parent[u] = p;
-  C.w.ds[u] = ods;
-  C.w.de[u] = x;
-  C.w.roff[u] = C.w.roff[y];
-  C.w.ftok[u] = C.w.ftok[y];
-  C.w.flags[u] = stateful ? F_SSM : 0u;
-  C.w.t[u] = r;
-  C.w.nchild[u] = 1;
-  C.w.cxor[u] = y;
-  C.w.hval[hash_index_1(C, hkey_of(p, C.w.ftok[u]))] = u;  // same key, new child
-  C.w.ds[y] = x;
-  const uint32_t ft = P.tok[C.w.roff[y] + x];
-  C.w.ftok[y] = ft;
-  C.w.parent[y] = u;
+  const uint32_t p = C.w.parent()[y];
+  const uint32_t ods = C.w.ds()[y];
+  C.w.id()[u] = C.next_id++;
+  C.w.parent()[u] = p;
+  C.w.ds()[u] = ods;
+  C.w.de()[u] = x;
+  C.w.roff()[u] = C.w.roff()[y];
+  C.w.ftok()[u] = C.w.ftok()[y];
+  C.w.flags()[u] = stateful ? F_SSM : 0u;
+  C.w.t()[u] = r;
+  C.w.nchild()[u] = 1;
+  C.w.cxor()[u] = y;
+  C.w.hval()[hash_index_1(C, hkey_of(p, C.w.ftok()[u]))] = u;  // same key, new child
+  C.w.ds()[y] = x;
+  const uint32_t ft = P.tok[C.w.roff()[y] + x];
+  C.w.ftok()[y] = ft;
+  C.w.parent()[y] = u;
   hash_insert_1(C, hkey_of(u, ft), y);
-  C.w.cxor[p] ^= y ^ u;
+  C.w.cxor()[p] ^= y ^ u;
   dense_add_1(C, u);
   dense_set_eff_1(C, y);
   C.c_wr += 2;
@@ -592,8 +704,8 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
 }
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
-  C.w.flags[x] |= F_SSM;
-  C.w.t[x] = r;
+  C.w.flags()[x] |= F_SSM;
+  C.w.t()[x] = r;
   dense_set_eff_1(C, x);
   dense_refresh_1(C, x);
   C.c_wr += 1;
@@ -626,15 +738,15 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     const uint32_t tk = __ldg(P.tok + off + pos);
     const uint32_t c = hash_find_warp(C, v, tk);
     if (c == NIL) { m = pos; break; }
-    const uint32_t ds = C.w.ds[c], de = C.w.de[c], fl = C.w.flags[c];
-    const uint64_t ro = C.w.roff[c];
+    const uint32_t ds = C.w.ds()[c], de = C.w.de()[c], fl = C.w.flags()[c];
+    const uint64_t ro = C.w.roff()[c];
     const uint32_t len = de - ds;
     const uint32_t cmp = min(len, n - pos);
     const uint32_t k = match_len(P.tok, ro + ds, off + pos, cmp);
     if (lane == 0) {
-      C.w.path[npath] = c;
-      C.w.flags[c] = fl | F_PIN;   // pin the path (R12)
-      C.w.dense[C.w.dpos[c]].tc |= NOTC;
+      C.w.path()[npath] = c;
+      C.w.flags()[c] = fl | F_PIN;   // pin the path (R12)
+      C.w.dense()[C.w.dpos()[c]].tc |= NOTC;
     }
     npath++;
     pinned_bytes += node_bytes(C.m, ds, de, fl & F_SSM);
@@ -659,8 +771,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     reuse = min(m, L_in);
     hit = NIL;
     for (uint32_t i = 0; i < npath; i++) {
-      const uint32_t x = C.w.path[i];
-      if (C.w.ds[x] < reuse) hit = x;
+      const uint32_t x = C.w.path()[i];
+      if (C.w.ds()[x] < reuse) hit = x;
     }
   }
 
@@ -670,7 +782,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   if (m_in > 0) {
     if (m >= L_in) {
       if (lin_bnd != NIL) {
-        if (!(C.w.flags[lin_bnd] & F_SSM)) { p = m_in; p_gain = lin_bnd; }
+        if (!(C.w.flags()[lin_bnd] & F_SSM)) { p = m_in; p_gain = lin_bnd; }
       } else {
         p = m_in;
         p_split = lin_node;
@@ -678,7 +790,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     } else if (partial != NIL) {
       p = m_in;
       p_split = partial;
-    } else if (!(C.w.flags[v] & F_SSM)) {
+    } else if (!(C.w.flags()[v] & F_SSM)) {
       p = m_in;
       p_gain = v;
     }
@@ -688,7 +800,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   const bool split_m = partial != NIL && m < n && m != p;   // stateless output-region split (R10)
   const bool split_n = partial != NIL && m == n && n != p;  // sequence ends inside an edge
   uint32_t n_gain = NIL;
-  if (partial == NIL && m == n && n != p && !(C.w.flags[v] & F_SSM)) n_gain = v;
+  if (partial == NIL && m == n && n != p && !(C.w.flags()[v] & F_SSM)) n_gain = v;
   uint32_t n_ck = p ? 1u : 0u;
   if (n != p && (leaf || split_n || n_gain != NIL)) n_ck++;
   const uint64_t d_bytes = C.m.kvt * (uint64_t)(n - m) + C.m.ssmb * n_ck;
@@ -697,7 +809,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   // Step 5: touch only the hit node.
   if (hit != NIL) {
     if (lane == 0) {
-      C.w.t[hit] = r;
+      C.w.t()[hit] = r;
       dense_refresh_1(C, hit);
     }
     C.c_wr += 1;
@@ -724,27 +836,27 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
       if (leaf && !C.failed) {
         const uint32_t w = alloc_1(C, P.status);
         if (w != NIL) {
-          C.w.id[w] = C.next_id++;
-          C.w.parent[w] = attach;
-          C.w.ds[w] = m;
-          C.w.de[w] = n;
-          C.w.roff[w] = off;
+          C.w.id()[w] = C.next_id++;
+          C.w.parent()[w] = attach;
+          C.w.ds()[w] = m;
+          C.w.de()[w] = n;
+          C.w.roff()[w] = off;
           const uint32_t ft = P.tok[off + m];
-          C.w.ftok[w] = ft;
-          C.w.flags[w] = F_SSM;
-          C.w.t[w] = r;
-          C.w.nchild[w] = 0;
-          C.w.cxor[w] = 0;
+          C.w.ftok()[w] = ft;
+          C.w.flags()[w] = F_SSM;
+          C.w.t()[w] = r;
+          C.w.nchild()[w] = 0;
+          C.w.cxor()[w] = 0;
           hash_insert_1(C, hkey_of(attach, ft), w);
-          C.w.nchild[attach] += 1;
-          C.w.cxor[attach] ^= w;
+          C.w.nchild()[attach] += 1;
+          C.w.cxor()[attach] ^= w;
           if (attach != 0) dense_refresh_1(C, attach);
           dense_add_1(C, w);
           C.c_wr += 1;
         }
       } else if (partial == NIL) {
         // final node at n already exists: timestamp it (R5)
-        C.w.t[v] = r;
+        C.w.t()[v] = r;
         dense_refresh_1(C, v);
         if (n_gain == NIL && p_gain != v) C.c_wr += 1;
       }
@@ -759,8 +871,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   // Step 9: unpin, outputs.
   if (lane == 0) {
     for (uint32_t i = 0; i < npath; i++) {
-      const uint32_t x = C.w.path[i];
-      C.w.flags[x] &= ~F_PIN;
+      const uint32_t x = C.w.path()[i];
+      C.w.flags()[x] &= ~F_PIN;
       dense_refresh_1(C, x);
     }
     if (reuse > L_in) {

@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmarconi.so")
+LIB_PATH = os.environ.get("MARCONI_LIB") or os.path.join(HERE, "libmarconi.so")
 
 # ---- struct layouts (must match include/marconi.h) ----
 REQUEST_DTYPE = np.dtype([("tok_off", "<u8"), ("input_len", "<u4"), ("output_len", "<u4")])
