@@ -145,7 +145,10 @@ mc_status mc_get_snapshot(mc_ctx* ctx, uint32_t variant, uint32_t k, mc_snap_nod
 /* Replay windows.  Chain c = ((variant * n_alpha) + alpha_idx) * n_segs + seg. */
 mc_status mc_set_segments(mc_ctx* ctx, const mc_segment* h_segs, uint32_t n_segs);
 
-/* Workspace bytes for `n_workers` concurrent chains (one warp each; 0 = the
+/* Workspaces (d_workspace of mc_replay / mc_live_pass) must be ZERO-INITIALISED
+ * by the caller when first allocated; they may then be reused across calls of
+ * the same context without clearing.
+ * Workspace bytes for `n_workers` concurrent chains (one warp each; 0 = the
  * default: every SM filled at the kernel's occupancy) and up to n_chains chain
  * ids per mc_replay call (0 = every chain of n_alpha α values). */
 mc_status mc_workspace_size(const mc_ctx* ctx, uint32_t n_workers, uint32_t n_alpha, uint32_t n_chains,
@@ -173,6 +176,8 @@ typedef struct {
   uint32_t* d_log_n;        /* [n_chains_total] records produced (may exceed log_cap)  */
   uint32_t* d_chain_ns;     /* [n_chains_total] nullable: per-chain clock64 cycles      */
   uint32_t n_workers;       /* 0 = default (derived from the workspace size)          */
+  uint32_t smem_nodes;      /* dense live-list positions per chain held in shared
+                               memory (0 = auto: fill the SM at the target occupancy) */
 } mc_replay_args;
 
 /* Run the chains (asynchronous on `stream`).  Each chain loads its snapshot,

@@ -37,7 +37,7 @@ mc_status fail(mc_status s, const std::string& m) {
   } while (0)
 
 #ifndef MC_MINBLOCKS
-#define MC_MINBLOCKS 4
+#define MC_MINBLOCKS 3
 #endif
 constexpr int kWarpsPerCta = 4;
 }  // namespace
@@ -46,6 +46,7 @@ constexpr int kWarpsPerCta = 4;
 // Kernels
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel(KParams P) {
+  extern __shared__ __align__(16) char smem[];
   const uint32_t lane = lane_id();
   const uint32_t worker = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (worker >= P.n_workers) return;
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const DevVariant V = P.var[v];
     const mc_segment seg = P.segs[s];
     Chain C;
-    chain_init(C, P, worker, V, P.alphas[a]);
+    chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 12ull * P.smem_nodes, P.smem_nodes);
     load_snapshot(C, P, &P.snap[v], seg.snapshot);
     mc_evict_rec* log = P.log ? P.log + (uint64_t)c * P.log_cap : nullptr;
     uint32_t* log_n = P.log ? P.log_n + c : nullptr;
@@ -82,10 +83,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     if (lane == 0) {
       atomicAdd(P.hit_sum + (uint64_t)v * P.n_alpha + a, sum);
       if (P.counters) {
+#if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
+        P.counters[4ull * c + 0] = C.t_walk;
+        P.counters[4ull * c + 1] = C.t_evict;
+        P.counters[4ull * c + 2] = C.t_insert;
+        P.counters[4ull * c + 3] = C.t_unpin;
+#else
         P.counters[4ull * c + 0] = C.c_cmp;
         P.counters[4ull * c + 1] = C.c_vis;
         P.counters[4ull * c + 2] = C.c_scan;
         P.counters[4ull * c + 3] = C.c_wr;
+#endif
       }
       if (P.chain_cycles) P.chain_cycles[c] = (uint32_t)min((long long)0xFFFFFFFF, (clock64() - t0) >> 10);
     }
@@ -94,11 +102,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
 }
 
 __global__ void __launch_bounds__(32) live_kernel(KParams P) {
+  extern __shared__ __align__(16) char smem[];
   const uint32_t lane = lane_id();
   const uint32_t v = blockIdx.x;
   if (v >= P.n_var) return;
   Chain C;
-  chain_init(C, P, v, P.var[v], 0.0);
+  chain_init(C, P, v, P.var[v], 0.0, smem, P.smem_nodes);
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
@@ -197,6 +206,9 @@ struct mc_ctx {
   int device = 0;
   int n_sm = 0;
   int blocks_per_sm = 1;
+  uint32_t smem_nodes = 0;       // default dense positions per warp in shared memory (replay)
+  uint32_t smem_nodes_live = 0;  // same for the 1-warp live-pass CTAs
+  uint64_t smem_optin = 0;
   uint32_t ncap = 0, hcap = 0;
   std::vector<mc_variant> hv;
   std::vector<DevVariant> dvh;
@@ -279,8 +291,24 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     return fail(MC_ECUDA, "cudaGetDeviceProperties failed");
   }
   c->n_sm = prop.multiProcessorCount;
+  // Shared memory: fill each SM with MC_MINBLOCKS CTAs of kWarpsPerCta warps; each
+  // warp keeps the first S dense positions (12 B each) of its chain on chip.
+  int smem_sm = 0, smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  c->smem_optin = (uint64_t)smem_optin;
+  {
+    const int64_t per_cta = std::min<int64_t>(smem_optin, smem_sm / MC_MINBLOCKS - 1024);
+    const int64_t per_warp = per_cta / kWarpsPerCta;
+    c->smem_nodes = (uint32_t)std::max<int64_t>(0, (per_warp / 12) & ~31ll);
+    c->smem_nodes = std::min<uint32_t>(c->smem_nodes, max_nodes);
+    c->smem_nodes_live = std::min<uint32_t>((uint32_t)((smem_optin / 12) & ~31), max_nodes);
+  }
+  cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(live_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel, 32 * kWarpsPerCta, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel, 32 * kWarpsPerCta,
+                                                kWarpsPerCta * 12ull * c->smem_nodes);
   c->blocks_per_sm = std::max(1, bps);
   c->ncap = max_nodes;
   c->hcap = 2 * max_nodes;
@@ -327,6 +355,7 @@ mc_status mc_set_trace(mc_ctx* c, const uint32_t* d_tokens, uint64_t n_tokens, c
                        uint32_t n_reqs) {
   if (!c || !d_tokens || !d_reqs || n_reqs == 0) return fail(MC_EINVAL, "mc_set_trace: null/empty argument");
   if (n_reqs >= (1u << 31)) return fail(MC_EINVAL, "too many requests (timestamps must stay < 2^31)");
+  if (n_tokens > 0xFFFFFFFFull) return fail(MC_EINVAL, "token pool must hold < 2^32 tokens (u32 node offsets)");
   std::vector<mc_request> h(n_reqs);
   CU(cudaMemcpy(h.data(), d_reqs, sizeof(mc_request) * n_reqs, cudaMemcpyDeviceToHost));
   for (uint32_t i = 0; i < n_reqs; i++) {
@@ -484,7 +513,8 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
   P.status = c->d_status;
   P.live_out = d_outs;
   P.window = window;
-  live_kernel<<<nv, 32, 0, st>>>(P);
+  P.smem_nodes = c->smem_nodes_live;
+  live_kernel<<<nv, 32, 12ull * c->smem_nodes_live, st>>>(P);
   CU(cudaGetLastError());
   // the last snapshot offset entry (K) for completeness
   std::vector<uint64_t> offK(1, (uint64_t)K * c->ncap);
@@ -603,8 +633,12 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   P.log_n = A->d_log_n;
   P.chain_cycles = A->d_chain_ns;
   P.status = c->d_status;
+  uint32_t S = A->smem_nodes ? A->smem_nodes : c->smem_nodes;
+  S = std::min<uint32_t>(S, c->ncap) & ~31u;
+  if (kWarpsPerCta * 12ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
+  P.smem_nodes = S;
   const uint32_t ctas = (workers + kWarpsPerCta - 1) / kWarpsPerCta;
-  replay_kernel<<<ctas, 32 * kWarpsPerCta, 0, st>>>(P);
+  replay_kernel<<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 12ull * S, st>>>(P);
   CU(cudaGetLastError());
   return MC_OK;
 }

@@ -1,22 +1,28 @@
 // replay.cuh -- device code of the Marconi α-grid replay (sm_100a).
 //
 // One WARP owns one chain (variant, α, segment): a private flattened radix
-// tree in a global-memory workspace slice, replayed request by request.
+// tree replayed request by request.
+//
+// Data layout per chain:
+//   shared memory  dense live-node list: t_last|NOTC (u32) and FLOP efficiency
+//                  (f64) for positions < S -- the data every eviction scans;
+//   global (L2)    32-byte AoS node records {parent, first token, d_start, d_end |
+//                  id, child xor, nchild|flags, dense position}, u32 pool offsets,
+//                  a 4-byte-entry open-addressing child index keyed by (parent,
+//                  first token) whose entries carry a generation tag (no table
+//                  clear between chains), the dense tail (positions >= S).
 // Warp-cooperative stages:
-//   K2 walk      -- child lookup = 32-wide linear-probe window of an
-//                   open-addressing hash keyed by (parent slot, first token);
-//                   edge compare = 128 tokens per step, coalesced loads +
-//                   __ballot_sync/__ffs for the first mismatch (PAPER:246,
+//   K2 walk      -- child lookup = 32-wide linear-probe window (one 128 B line of
+//                   entries + the candidates' records in parallel); edge compare =
+//                   128 tokens per step with __ballot_sync/__ffs (PAPER:246,
 //                   PAPER:300-301; speculative insertion PAPER:365 fused in);
-//   K3 scan      -- one pass over the dense live-node list for the min/max
-//                   normalisation bounds, one pass for the lexicographic
-//                   (u, t_last, id) argmin of Eq. 2, both
-//                   reduced with warp shuffles;
+//   K3 scan      -- normalisation bounds + filter-and-verify argmin of Eq. 2
+//                   (PAPER:414-419), warp-shuffle reductions;
 //   snapshot load / dump -- 32 nodes per step.
 // Scalar tree mutations (K4: split, leaf, gain, leaf removal, absorption --
-// PAPER:362-365) run on lane 0 with the chain's scalar state
-// broadcast afterwards.  K1 (Eq. 1 cost model, Appendix A) is inlined at
-// every node create/split/merge/gain.
+// PAPER:362-365) run on lane 0; the chain scalars are then
+// broadcast.  K1 (Eq. 1 cost model, Appendix A) is inlined wherever a node's
+// range or state changes.
 //
 // Bit-exactness: integer FLOPs/bytes are exact u64; eff = one IEEE division;
 // the utility uses __dsub_rn/__ddiv_rn/__dmul_rn/__dadd_rn (no FMA).
@@ -28,9 +34,10 @@
 namespace mcd {
 
 constexpr uint32_t NIL = 0xFFFFFFFFu;
-constexpr unsigned long long EMPTY = ~0ull;
-constexpr uint32_t NOTC = 0x80000000u;  // dense record: not an eviction candidate
-constexpr uint32_t F_SSM = 1u, F_PIN = 2u;
+constexpr uint32_t NOTC = 0x80000000u;  // dense tc: not an eviction candidate
+constexpr uint32_t F_SSM = 1u, F_PIN = 2u;  // node flags (bits 24.. of NodeRec::nf)
+constexpr uint32_t NCH_MASK = 0x00FFFFFFu;
+constexpr uint32_t SLOT_BITS = 20, SLOT_MASK = (1u << SLOT_BITS) - 1, GEN_MAX = 4095;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 // device status word bits (mc_check)
@@ -73,10 +80,15 @@ struct DevSnapOut {
   uint32_t count, pad;
 };
 
-struct __align__(16) DenseRec {
+struct __align__(16) DenseRec {  // global tail of the dense list (positions >= S)
   uint32_t tc;  // t_last | NOTC
-  uint32_t id;
+  uint32_t pad;
   double eff;
+};
+
+struct __align__(16) NodeRec {
+  uint32_t parent, ftok, ds, de;  // first 16 B: what the walk and the child index read
+  uint32_t id, cxor, nf, dpos;    // nf = nchild (bits 0..23) | flags << 24
 };
 
 struct KParams {
@@ -107,48 +119,33 @@ struct KParams {
   // live pass
   DevSnapOut* live_out;
   uint32_t window;
+  uint32_t smem_nodes;  // dense positions held in shared memory per warp
 };
 
-// Per-worker workspace slice (SoA node table + dense live list + hash).  Only the
-// base pointer and sizes live in registers; array addresses are recomputed.
+// Per-worker workspace slice.  The caller zero-initialises the workspace once
+// (header word 0 = child-index generation, word 1 = layout signature).
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
-  uint64_t b = 14ull * 4 * ncap  // 13 u32 node arrays (+1 spare)
-               + 8ull * ncap     // roff
-               + 16ull * ncap    // dense
-               + 12ull * hcap;   // hkey + hval
+  uint64_t b = 256                  // header
+               + 32ull * ncap       // node records
+               + 4ull * ncap        // roff (u32)
+               + 4ull * hcap        // child index
+               + 12ull * ncap       // dslot, path, freel
+               + 16ull * ncap;      // dense tail
   return (b + 255) & ~255ull;
 }
 
 struct WS {
   char* b;
   uint32_t n, h;
-  __device__ __forceinline__ DenseRec* dense() const { return (DenseRec*)b; }
-  __device__ __forceinline__ uint64_t* roff() const { return (uint64_t*)(b + 16ull * n); }
-  __device__ __forceinline__ unsigned long long* hkey() const { return (unsigned long long*)(b + 24ull * n); }
-  __device__ __forceinline__ uint32_t* a32(uint32_t k) const { return (uint32_t*)(b + 24ull * n + 8ull * h + 4ull * k * n); }
-  __device__ __forceinline__ uint32_t* id() const { return a32(0); }
-  __device__ __forceinline__ uint32_t* parent() const { return a32(1); }
-  __device__ __forceinline__ uint32_t* ds() const { return a32(2); }
-  __device__ __forceinline__ uint32_t* de() const { return a32(3); }
-  __device__ __forceinline__ uint32_t* t() const { return a32(4); }
-  __device__ __forceinline__ uint32_t* nchild() const { return a32(5); }
-  __device__ __forceinline__ uint32_t* cxor() const { return a32(6); }
-  __device__ __forceinline__ uint32_t* ftok() const { return a32(7); }
-  __device__ __forceinline__ uint32_t* flags() const { return a32(8); }
-  __device__ __forceinline__ uint32_t* dpos() const { return a32(9); }
-  __device__ __forceinline__ uint32_t* dslot() const { return a32(10); }
-  __device__ __forceinline__ uint32_t* path() const { return a32(11); }
-  __device__ __forceinline__ uint32_t* freel() const { return a32(12); }
-  __device__ __forceinline__ uint32_t* hval() const { return (uint32_t*)(b + 24ull * n + 8ull * h + 52ull * n); }
+  __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
+  __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
+  __device__ __forceinline__ uint32_t* roff() const { return (uint32_t*)(b + 256 + 32ull * n); }
+  __device__ __forceinline__ uint32_t* tab() const { return (uint32_t*)(b + 256 + 36ull * n); }
+  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n + 4ull * h); }
+  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n + 4ull * h); }
+  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n + 4ull * h); }
+  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 48ull * n + 4ull * h); }
 };
-
-__device__ inline WS ws_slice(char* base, uint32_t ncap, uint32_t hcap) {
-  WS w;
-  w.b = base;
-  w.n = ncap;
-  w.h = hcap;
-  return w;
-}
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -182,16 +179,17 @@ __device__ __forceinline__ void bounds_init(Bounds& b) {
 __device__ __forceinline__ void bounds_add(Bounds& b, uint32_t t, double e) {
   b.tmin = min(b.tmin, t);
   b.tmax = max(b.tmax, t);
-  b.emin = fmin(b.emin, e);
-  b.emax = fmax(b.emax, e);
+  b.emin = e < b.emin ? e : b.emin;  // eff is finite and positive: no NaN handling needed
+  b.emax = e > b.emax ? e : b.emax;
 }
 __device__ __forceinline__ void bounds_reduce(Bounds& b) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     b.tmin = min(b.tmin, __shfl_xor_sync(FULL, b.tmin, o));
     b.tmax = max(b.tmax, __shfl_xor_sync(FULL, b.tmax, o));
-    b.emin = fmin(b.emin, __shfl_xor_sync(FULL, b.emin, o));
-    b.emax = fmax(b.emax, __shfl_xor_sync(FULL, b.emax, o));
+    const double lo = __shfl_xor_sync(FULL, b.emin, o), hi = __shfl_xor_sync(FULL, b.emax, o);
+    b.emin = lo < b.emin ? lo : b.emin;
+    b.emax = hi > b.emax ? hi : b.emax;
   }
 }
 // u = rec + α·effn, each operation rounded (no FMA); degenerate range -> 0.5 (R2).
@@ -231,7 +229,10 @@ __device__ __forceinline__ void best_reduce(Best& b) {
 // ---------------------------------------------------------------------------
 struct Chain {
   WS w;
-  uint32_t ncap, hmask;
+  uint32_t* stc;    // SMEM: dense t_last|NOTC for positions < S
+  double* seff;     // SMEM: dense eff for positions < S
+  uint32_t S;       // SMEM-resident dense positions (the tail lives in global)
+  uint32_t ncap, hmask, gen;
   uint32_t count;     // live non-root nodes (= dense list length)
   uint64_t total;     // bytes of all live nodes
   uint32_t next_id, hwm, nfree;
@@ -240,6 +241,9 @@ struct Chain {
   uint32_t capn;
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
+#if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
+  unsigned long long t_walk, t_evict, t_insert, t_unpin;
+#endif
   bool failed;
 };
 
@@ -254,7 +258,8 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.failed = __shfl_sync(FULL, (int)C.failed, 0);
 }
 
-__device__ __forceinline__ uint32_t hslot(unsigned long long key, uint32_t mask) {
+__device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_t mask) {
+  unsigned long long key = ((unsigned long long)parent << 32) | tok;
   key ^= key >> 33;
   key *= 0xff51afd7ed558ccdull;
   key ^= key >> 33;
@@ -262,23 +267,30 @@ __device__ __forceinline__ uint32_t hslot(unsigned long long key, uint32_t mask)
   key ^= key >> 33;
   return (uint32_t)key & mask;
 }
-__device__ __forceinline__ unsigned long long hkey_of(uint32_t parent, uint32_t tok) {
-  return ((unsigned long long)parent << 32) | tok;
-}
+__device__ __forceinline__ bool hvalid(const Chain& C, uint32_t e) { return (e >> SLOT_BITS) == C.gen; }
+__device__ __forceinline__ uint32_t hentry(const Chain& C, uint32_t slot) { return (C.gen << SLOT_BITS) | slot; }
 
-// Warp-cooperative lookup of child(parent, tok): 32 probe positions per step.
+// Warp-cooperative lookup of child(parent, tok): 32 probe positions per step; the
+// key of an entry is its node record's (parent, first token).
 __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t parent, uint32_t tok) {
-  const unsigned long long key = hkey_of(parent, tok);
-  const uint32_t h = hslot(key, C.hmask);
+  const uint32_t h = hslot(parent, tok, C.hmask);
   const uint32_t lane = lane_id();
+  const uint32_t* __restrict__ tab = C.w.tab();
+  const NodeRec* __restrict__ rec = C.w.rec();
   for (uint32_t base = 0; base <= C.hmask; base += 32) {
-    const uint32_t idx = (h + base + lane) & C.hmask;
-    const unsigned long long k = C.w.hkey()[idx];
-    const unsigned mm = __ballot_sync(FULL, k == key);
-    const unsigned me = __ballot_sync(FULL, k == EMPTY);
+    const uint32_t e = tab[(h + base + lane) & C.hmask];
+    const bool valid = hvalid(C, e);
+    bool hit = false;
+    if (valid) {
+      const uint2 pf = *reinterpret_cast<const uint2*>(&rec[e & SLOT_MASK]);
+      hit = pf.x == parent && pf.y == tok;
+    }
+    const unsigned mm = __ballot_sync(FULL, hit);
+    const unsigned me = __ballot_sync(FULL, !valid);
     if (mm) {
       const int fm = __ffs(mm) - 1;
-      if (!me || fm < __ffs(me) - 1) return C.w.hval()[(h + base + fm) & C.hmask];
+      const uint32_t slot = __shfl_sync(FULL, e & SLOT_MASK, fm);
+      if (!me || fm < __ffs(me) - 1) return slot;
       return NIL;
     }
     if (me) return NIL;
@@ -286,66 +298,76 @@ __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t pare
   return NIL;
 }
 
-// ---- single-thread (lane 0) hash mutations: linear probing, backward-shift delete ----
-__device__ __forceinline__ uint32_t hash_index_1(const Chain& C, unsigned long long key) {
-  uint32_t i = hslot(key, C.hmask);
+// ---- single-thread (lane 0) child-index mutations: linear probing, backward-shift delete ----
+__device__ __forceinline__ uint32_t hash_index_1(const Chain& C, uint32_t parent, uint32_t tok) {
+  uint32_t i = hslot(parent, tok, C.hmask);
   for (;;) {
-    unsigned long long k = C.w.hkey()[i];
-    if (k == key) return i;
-    if (k == EMPTY) return NIL;
+    const uint32_t e = C.w.tab()[i];
+    if (!hvalid(C, e)) return NIL;
+    const NodeRec& R = C.w.rec()[e & SLOT_MASK];
+    if (R.parent == parent && R.ftok == tok) return i;
     i = (i + 1) & C.hmask;
   }
 }
-__device__ __forceinline__ void hash_insert_1(Chain& C, unsigned long long key, uint32_t val) {
-  uint32_t i = hslot(key, C.hmask);
-  while (C.w.hkey()[i] != EMPTY) i = (i + 1) & C.hmask;
-  C.w.hkey()[i] = key;
-  C.w.hval()[i] = val;
+__device__ __forceinline__ void hash_insert_1(Chain& C, uint32_t parent, uint32_t tok, uint32_t slot) {
+  uint32_t i = hslot(parent, tok, C.hmask);
+  while (hvalid(C, C.w.tab()[i])) i = (i + 1) & C.hmask;
+  C.w.tab()[i] = hentry(C, slot);
 }
 __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & C.hmask;
-    unsigned long long k = C.w.hkey()[j];
-    if (k == EMPTY) break;
-    uint32_t home = hslot(k, C.hmask);
-    bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
+    const uint32_t e = C.w.tab()[j];
+    if (!hvalid(C, e)) break;
+    const NodeRec& R = C.w.rec()[e & SLOT_MASK];
+    const uint32_t home = hslot(R.parent, R.ftok, C.hmask);
+    const bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
     if (!stays) {
-      C.w.hkey()[i] = k;
-      C.w.hval()[i] = C.w.hval()[j];
+      C.w.tab()[i] = e;
       i = j;
     }
   }
-  C.w.hkey()[i] = EMPTY;
+  C.w.tab()[i] = 0;
 }
 
-// ---- dense live list (lane 0) ----
-__device__ __forceinline__ void dense_refresh_1(Chain& C, uint32_t s) {
-  const bool cand = C.w.nchild()[s] <= 1 && !(C.w.flags()[s] & F_PIN);
-  C.w.dense()[C.w.dpos()[s]].tc = C.w.t()[s] | (cand ? 0u : NOTC);
+// ---- dense live list: positions < S in shared memory, the tail in global ----
+__device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return i < C.S ? C.stc[i] : C.w.tail()[i].tc; }
+__device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return i < C.S ? C.seff[i] : C.w.tail()[i].eff; }
+__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.rec()[C.w.dslot()[i]].id; }
+__device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) {
+  if (i < C.S) C.stc[i] = v; else C.w.tail()[i].tc = v;
 }
-__device__ __forceinline__ void dense_set_eff_1(Chain& C, uint32_t s) {
-  C.w.dense()[C.w.dpos()[s]].eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
+__device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
+  if (i < C.S) C.seff[i] = v; else C.w.tail()[i].eff = v;
 }
-__device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s) {
+__device__ __forceinline__ bool is_cand(uint32_t nf) { return (nf & NCH_MASK) <= 1 && !((nf >> 24) & F_PIN); }
+// (re)write node s's dense tc with timestamp t (lane 0)
+__device__ __forceinline__ void set_t_1(Chain& C, uint32_t s, uint32_t t) {
+  const NodeRec& R = C.w.rec()[s];
+  d_set_tc(C, R.dpos, t | (is_cand(R.nf) ? 0u : NOTC));
+}
+__device__ __forceinline__ void refresh_1(Chain& C, uint32_t s) {
+  const NodeRec& R = C.w.rec()[s];
+  d_set_tc(C, R.dpos, (d_tc(C, R.dpos) & ~NOTC) | (is_cand(R.nf) ? 0u : NOTC));
+}
+__device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   const uint32_t i = C.count++;
-  C.w.dpos()[s] = i;
+  NodeRec& R = C.w.rec()[s];
+  R.dpos = i;
   C.w.dslot()[i] = s;
-  DenseRec d;
-  d.tc = 0;
-  d.id = C.w.id()[s];
-  d.eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
-  C.w.dense()[i] = d;
-  dense_refresh_1(C, s);
+  d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
+  d_set_tc(C, i, t | (is_cand(R.nf) ? 0u : NOTC));
 }
 __device__ __forceinline__ void dense_remove_1(Chain& C, uint32_t s) {
-  const uint32_t i = C.w.dpos()[s];
+  const uint32_t i = C.w.rec()[s].dpos;
   const uint32_t last = --C.count;
   if (i != last) {
-    C.w.dense()[i] = C.w.dense()[last];
+    d_set_tc(C, i, d_tc(C, last));
+    d_set_eff(C, i, d_eff(C, last));
     const uint32_t s2 = C.w.dslot()[last];
     C.w.dslot()[i] = s2;
-    C.w.dpos()[s2] = i;
+    C.w.rec()[s2].dpos = i;
   }
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
@@ -377,51 +399,71 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     C.failed = true;
     return;
   }
-  for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.hkey()[i] = EMPTY;
-  for (uint32_t i = lane; i <= n; i += 32) {
-    C.w.nchild()[i] = 0;
-    C.w.cxor()[i] = 0;
-  }
+  // child-index generation: entries of earlier chains on this worker become stale
+  uint32_t g = 0;
+  bool clear = false;
   if (lane == 0) {
-    C.w.id()[0] = 0; C.w.parent()[0] = NIL; C.w.ds()[0] = 0; C.w.de()[0] = 0; C.w.t()[0] = 0;
-    C.w.flags()[0] = 0; C.w.roff()[0] = 0; C.w.ftok()[0] = 0;
+    uint32_t* hd = C.w.hdr();
+    g = hd[0] + 1;
+    if (g > GEN_MAX || hd[1] != C.ncap) {
+      clear = true;
+      g = 1;
+      hd[1] = C.ncap;
+    }
+    hd[0] = g;
   }
+  g = __shfl_sync(FULL, g, 0);
+  clear = __shfl_sync(FULL, (int)clear, 0);
+  if (clear)
+    for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.tab()[i] = 0;
+  C.gen = g;
   __syncwarp();
+  if (lane == 0) {
+    NodeRec z;
+    z.parent = NIL; z.ftok = 0; z.ds = 0; z.de = 0; z.id = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
+    C.w.rec()[0] = z;
+  }
   uint64_t bytes = 0;
   bool bad = false;
   for (uint32_t i = lane; i < n; i += 32) {
     const mc_snap_node r = nodes[i];
     const uint32_t s = i + 1;
     const uint32_t pi = pidx[i];
-    const uint32_t ps = (pi == NIL) ? 0u : pi + 1;
     bad |= (r.d_end <= r.d_start) || (r.ref_off + r.d_end > P.n_tok) || (pi != NIL && pi >= n);
-    C.w.id()[s] = r.id;
-    C.w.parent()[s] = ps;
-    C.w.ds()[s] = r.d_start;
-    C.w.de()[s] = r.d_end;
-    C.w.t()[s] = r.t_last;
-    C.w.roff()[s] = r.ref_off;
-    C.w.flags()[s] = r.has_ssm ? F_SSM : 0u;
-    const uint32_t ft = P.tok[r.ref_off + r.d_start];
-    C.w.ftok()[s] = ft;
-    C.w.dpos()[s] = i;
+    NodeRec R;
+    R.parent = (pi == NIL) ? 0u : pi + 1;
+    R.ftok = P.tok[r.ref_off + r.d_start];
+    R.ds = r.d_start;
+    R.de = r.d_end;
+    R.id = r.id;
+    R.cxor = 0;
+    R.nf = (r.has_ssm ? F_SSM : 0u) << 24;
+    R.dpos = i;
+    C.w.rec()[s] = R;
+    C.w.roff()[s] = (uint32_t)r.ref_off;
     C.w.dslot()[i] = s;
-    atomicAdd(&C.w.nchild()[ps], 1u);
-    atomicXor(&C.w.cxor()[ps], s);
-    const unsigned long long key = hkey_of(ps, ft);
-    uint32_t j = hslot(key, C.hmask);
-    while (atomicCAS(&C.w.hkey()[j], EMPTY, key) != EMPTY) j = (j + 1) & C.hmask;
-    C.w.hval()[j] = s;
     bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
-    DenseRec d;
-    d.tc = C.w.t()[s] | (C.w.nchild()[s] <= 1 ? 0u : NOTC);
-    d.id = C.w.id()[s];
-    d.eff = node_eff(C.m, C.w.ds()[s], C.w.de()[s], C.w.flags()[s] & F_SSM);
-    C.w.dense()[i] = d;
+    const NodeRec& R = C.w.rec()[s];
+    const uint32_t ps = R.parent, ft = R.ftok;
+    atomicAdd(&C.w.rec()[ps].nf, 1u);
+    atomicXor(&C.w.rec()[ps].cxor, s);
+    uint32_t j = hslot(ps, ft, C.hmask);
+    for (;;) {
+      const uint32_t e = atomicAdd(&C.w.tab()[j], 0u);  // coherent read (other lanes insert concurrently)
+      if (hvalid(C, e)) { j = (j + 1) & C.hmask; continue; }
+      if (atomicCAS(&C.w.tab()[j], e, hentry(C, s)) == e) break;
+    }
+  }
+  __syncwarp();
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint32_t s = i + 1;
+    const NodeRec R = C.w.rec()[s];
+    d_set_tc(C, i, nodes[i].t_last | (is_cand(R.nf) ? 0u : NOTC));
+    d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(FULL, (unsigned long long)bytes, o);
@@ -449,17 +491,18 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
   uint32_t* pdst = out->pidx + (uint64_t)k * out->stride;
   for (uint32_t i = lane; i < C.count; i += 32) {
     const uint32_t s = C.w.dslot()[i];
-    const uint32_t p = C.w.parent()[s];
+    const NodeRec R = C.w.rec()[s];
+    const uint32_t p = R.parent;
     mc_snap_node r;
-    r.id = C.w.id()[s];
-    r.parent_id = (p == 0) ? 0u : C.w.id()[p];
+    r.id = R.id;
+    r.parent_id = (p == 0) ? 0u : C.w.rec()[p].id;
     r.ref_off = C.w.roff()[s];
-    r.d_start = C.w.ds()[s];
-    r.d_end = C.w.de()[s];
-    r.t_last = C.w.t()[s];
-    r.has_ssm = (C.w.flags()[s] & F_SSM) ? 1u : 0u;
+    r.d_start = R.ds;
+    r.d_end = R.de;
+    r.t_last = d_tc(C, i) & ~NOTC;
+    r.has_ssm = ((R.nf >> 24) & F_SSM) ? 1u : 0u;
     dst[i] = r;
-    pdst[i] = (p == 0) ? NIL : C.w.dpos()[p];
+    pdst[i] = (p == 0) ? NIL : C.w.rec()[p].dpos;
   }
   if (lane == 0) {
     out->off[k] = (uint64_t)k * out->stride;
@@ -490,50 +533,77 @@ __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, 
   return cmp;
 }
 
-// ---------------------------------------------------------------------------
-// K3 + K4: one eviction
-// ---------------------------------------------------------------------------
-// Exact victim selection over the dense live list (Eq. 2).
-//   α = 0: u = rec exactly and rec is strictly monotone in t, so the victim is
-//          the candidate with the smallest (t_last, id) -- one pass (LRU,
-//          PAPER:424); only the victim's u is computed.
-//   α > 0: filter and verify.  Pass 1: bounds.  Pass 2: a division-free
-//          approximate key k' = (t - tmin) * RN(1/Δt) + (e - emin) * RN(α/Δe)
-//          with |k' - u| <= 10 (1+α) 2^-53; each lane keeps its best two keys.
-//          Only entries with k' <= min k' + δ, δ = (1+α) 2^-45, can be the exact
-//          argmin; their exact u (the IEEE recipe) decides.  If any lane has
-//          two entries within δ (near-ties), fall back to the exact full pass.
 #ifndef MC_UNROLL
 #define MC_UNROLL 2
 #endif
 constexpr int kUnroll = MC_UNROLL;
 
-__device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b) {
+// Development build (-DMC_PHASE_TIMERS): the 4 per-chain counters record clock64
+// cycles spent in walk / plan+evict / insert / unpin+outputs instead.
+#ifdef MC_PHASE_TIMERS
+#define PHASE_T0() long long _pt = clock64()
+#define PHASE_MARK(ctr) do { long long _n = clock64(); ctr += (unsigned long long)(_n - _pt); _pt = _n; } while (0)
+#else
+#define PHASE_T0() do {} while (0)
+#define PHASE_MARK(ctr) do {} while (0)
+#endif
+
+// Visit every dense position i < cnt as f(i, tc, eff): shared-memory part first,
+// then the global tail; kUnroll independent loads in flight per lane.
+template <class F>
+__device__ __forceinline__ void scan_dense(const Chain& C, uint32_t cnt, F&& f) {
   const uint32_t lane = lane_id();
-  const DenseRec* __restrict__ dn = C.w.dense();
+  const uint32_t ns = min(cnt, C.S);
+  for (uint32_t base = 0; base < ns; base += 32 * kUnroll) {
+    uint32_t tc[kUnroll];
+    double e[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < ns) { tc[q] = C.stc[i]; e[q] = C.seff[i]; }
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < ns) f(i, tc[q], e[q]);
+    }
+  }
+  const DenseRec* __restrict__ dn = C.w.tail();
+  for (uint32_t base = ns; base < cnt; base += 32 * kUnroll) {
+    DenseRec d[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < cnt) d[q] = dn[i];
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      const uint32_t i = base + 32 * q + lane;
+      if (i < cnt) f(i, d[q].tc, d[q].eff);
+    }
+  }
+}
+
+__device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b) {
   Best best;
   best_init(best);
   bounds_init(b);
   if (C.alpha == 0.0) {
-    for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
-      DenseRec d[kUnroll];
-#pragma unroll
-      for (int q = 0; q < kUnroll; q++) {
-        const uint32_t i = base + 32 * q + lane;
-        if (i < cnt) d[q] = dn[i];
-      }
-#pragma unroll
-      for (int q = 0; q < kUnroll; q++) {
-        const uint32_t i = base + 32 * q + lane;
-        if (i >= cnt) continue;
-        const uint32_t t = d[q].tc & ~NOTC;
-        b.tmin = min(b.tmin, t);
-        b.tmax = max(b.tmax, t);
-        if (!(d[q].tc & NOTC) && (t < best.t || (t == best.t && d[q].id < best.id))) {
-          best.t = t; best.id = d[q].id; best.i = i;
+    scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double) {
+      const uint32_t t = tc & ~NOTC;
+      b.tmin = min(b.tmin, t);
+      b.tmax = max(b.tmax, t);
+      if (!(tc & NOTC) && t <= best.t) {
+        if (t < best.t) {
+          best.t = t; best.i = i; best.id = NIL;  // id fetched lazily on a t tie
+        } else {
+          if (best.id == NIL) best.id = d_id(C, best.i);
+          const uint32_t id = d_id(C, i);
+          if (id < best.id) { best.i = i; best.id = id; }
         }
       }
-    }
+    });
+    if (best.i != NIL && best.id == NIL) best.id = d_id(C, best.i);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       b.tmin = min(b.tmin, __shfl_xor_sync(FULL, b.tmin, o));
@@ -551,70 +621,70 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     }
     return best;
   }
+#ifdef MC_PHASE_TIMERS3
+  Chain& CC = const_cast<Chain&>(C);
+  long long _t3 = clock64();
+#define T3(ctr) do { long long _n3 = clock64(); CC.ctr += (unsigned long long)(_n3 - _t3); _t3 = _n3; } while (0)
+#else
+#define T3(ctr) do {} while (0)
+#endif
   // pass 1: bounds over ALL non-root nodes (R1)
-  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
-    DenseRec d[kUnroll];
-#pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < cnt) d[q] = dn[i];
-    }
-#pragma unroll
-    for (int q = 0; q < kUnroll; q++)
-      if (base + 32 * q + lane < cnt) bounds_add(b, d[q].tc & ~NOTC, d[q].eff);
-  }
+  scan_dense(C, cnt, [&](uint32_t, uint32_t tc, double e) { bounds_add(b, tc & ~NOTC, e); });
   bounds_reduce(b);
-  // pass 2: approximate keys, best two per lane
+  T3(t_walk);
+  // pass 2: approximate keys in fp32, best two per lane (branch-free).
+  //   k = (t - tmin) * RN(1/Δt) + (RN32(e) - RN32(emin)) * RN32(α/Δe)
+  //   |k - (u - const)| <= E = 2^-21 (1 + α (1 + emax/Δe)),
+  //   so the exact argmin has k <= kmin + δ with δ = 2^-19 (1 + α (1 + emax/Δe)).
   const bool dt0 = b.tmax == b.tmin, de0 = b.emax == b.emin;
-  const double idt = dt0 ? 0.0 : __drcp_rn((double)(b.tmax - b.tmin));
-  const double aide = de0 ? 0.0 : __ddiv_rn(C.alpha, __dsub_rn(b.emax, b.emin));
-  const double kconst = __dadd_rn(dt0 ? 0.5 : 0.0, de0 ? __dmul_rn(C.alpha, 0.5) : 0.0);
-  const double INF = __longlong_as_double(0x7FF0000000000000ll);
-  double k1 = INF, k2 = INF;
+  const double de64 = __dsub_rn(b.emax, b.emin);
+  const float idt = dt0 ? 0.0f : __frcp_rn((float)(b.tmax - b.tmin));
+  const float aide = de0 ? 0.0f : __double2float_rn(__ddiv_rn(C.alpha, de64));
+  const float emin32 = __double2float_rn(b.emin);
+  const float INF = __int_as_float(0x7F800000);
+  float k1 = INF, k2 = INF;
   uint32_t i1 = NIL;
-  for (uint32_t base = 0; base < cnt; base += 32 * kUnroll) {
-    DenseRec d[kUnroll];
+  scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double e) {
+    const float k = (tc & NOTC) ? INF
+                                : __fmaf_rn(__fsub_rn(__double2float_rn(e), emin32), aide,
+                                            __fmul_rn(__uint2float_rn(tc - b.tmin), idt));
+    const bool lt1 = k < k1, lt2 = k < k2;
+    k2 = lt1 ? k1 : (lt2 ? k : k2);
+    i1 = lt1 ? i : i1;
+    k1 = lt1 ? k : k1;
+  });
+  float kmin = k1;
 #pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < cnt) d[q] = dn[i];
-    }
-#pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i >= cnt || (d[q].tc & NOTC)) continue;
-      const double k = __dadd_rn(__dadd_rn(__dmul_rn((double)(d[q].tc - b.tmin), idt),
-                                           __dmul_rn(__dsub_rn(d[q].eff, b.emin), aide)), kconst);
-      if (k < k1) { k2 = k1; k1 = k; i1 = i; }
-      else if (k < k2) { k2 = k; }
-    }
-  }
-  double kmin = k1;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) kmin = fmin(kmin, __shfl_xor_sync(FULL, kmin, o));
+  for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
+  T3(t_evict);
   if (kmin == INF) return best;  // no candidate
-  const double delta = __dmul_rn(__dadd_rn(1.0, C.alpha), 2.842170943040401e-14);  // (1+α) 2^-45
-  const double lim = __dadd_rn(kmin, delta);
-  if (!__any_sync(FULL, k2 <= lim)) {
-    if (k1 <= lim) {
-      const DenseRec d = dn[i1];
-      best.u = utility(b, d.tc, d.eff, C.alpha);
-      best.t = d.tc;
-      best.id = d.id;
+  const double ratio = de0 ? 0.0 : __ddiv_rn(b.emax, de64);
+  const double delta = 1.9073486328125e-06 * (1.0 + C.alpha * (1.0 + ratio));  // 2^-19 (1 + α (1 + emax/Δe))
+  const double lim = (double)kmin + delta;
+  if (!__any_sync(FULL, (double)k2 <= lim)) {
+    if ((double)k1 <= lim) {
+      const uint32_t tc = d_tc(C, i1);
+      best.u = utility(b, tc, d_eff(C, i1), C.alpha);
+      best.t = tc;
+      best.id = d_id(C, i1);
       best.i = i1;
     }
     best_reduce(best);
+    T3(t_insert);
     return best;
   }
+#ifdef MC_PHASE_TIMERS3
+  CC.t_unpin += 1;  // number of exact fallback passes
+#endif
   // near-ties: exact full pass
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const DenseRec d = dn[i];
-    if (d.tc & NOTC) continue;
-    const double u = utility(b, d.tc, d.eff, C.alpha);
-    if (best.i == NIL || better(u, d.tc, d.id, best)) {
-      best.u = u; best.t = d.tc; best.id = d.id; best.i = i;
+  scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double e) {
+    if (tc & NOTC) return;
+    const double u = utility(b, tc, e, C.alpha);
+    const uint32_t id = d_id(C, i);
+    if (best.i == NIL || better(u, tc, id, best)) {
+      best.u = u; best.t = tc; best.id = id; best.i = i;
     }
-  }
+  });
   best_reduce(best);
   return best;
 }
@@ -623,7 +693,13 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
   const uint32_t lane = lane_id();
   const uint32_t cnt = C.count;
   Bounds b;
+#ifdef MC_PHASE_TIMERS2
+  long long _ts = clock64();
+#endif
   const Best best = select_victim(C, cnt, b);
+#ifdef MC_PHASE_TIMERS2
+  C.t_unpin += (unsigned long long)(clock64() - _ts);
+#endif
   C.c_scan += cnt;
   if (best.i == NIL) {
     if (lane == 0) atomicOr(P.status, ST_NOCAND);
@@ -632,28 +708,32 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
   }
   if (lane == 0) {
     const uint32_t x = C.w.dslot()[best.i];
-    const uint32_t p = C.w.parent()[x];
-    const uint32_t xf = C.w.flags()[x];
+    const NodeRec X = C.w.rec()[x];
+    const uint32_t p = X.parent;
+    const uint32_t xf = X.nf >> 24;
     uint32_t kind;
-    if (C.w.nchild()[x] == 0) {  // leaf: free KVs + state
+    if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
       kind = 0;
-      C.total -= node_bytes(C.m, C.w.ds()[x], C.w.de()[x], xf & F_SSM);
-      hash_erase_at_1(C, hash_index_1(C, hkey_of(p, C.w.ftok()[x])));
-      C.w.nchild()[p] -= 1;
-      C.w.cxor()[p] ^= x;
-      if (p != 0) dense_refresh_1(C, p);
+      C.total -= node_bytes(C.m, X.ds, X.de, xf & F_SSM);
+      hash_erase_at_1(C, hash_index_1(C, p, X.ftok));
+      NodeRec& Rp = C.w.rec()[p];
+      Rp.nf -= 1;
+      Rp.cxor ^= x;
+      if (p != 0) refresh_1(C, p);
       C.c_wr += 1;
-    } else {  // one child: release the state, the child absorbs the KVs
+    } else {  // one child: release the state, the child absorbs the KVs (PAPER:435)
       kind = 1;
-      const uint32_t c = C.w.cxor()[x];
+      const uint32_t c = X.cxor;
+      NodeRec& Rc = C.w.rec()[c];
       if (xf & F_SSM) C.total -= C.m.ssmb;
-      hash_erase_at_1(C, hash_index_1(C, hkey_of(x, C.w.ftok()[c])));
-      C.w.hval()[hash_index_1(C, hkey_of(p, C.w.ftok()[x]))] = c;
-      C.w.ds()[c] = C.w.ds()[x];
-      C.w.ftok()[c] = C.w.ftok()[x];
-      C.w.parent()[c] = p;
-      C.w.cxor()[p] ^= x ^ c;
-      dense_set_eff_1(C, c);
+      hash_erase_at_1(C, hash_index_1(C, x, Rc.ftok));
+      const uint32_t hi = hash_index_1(C, p, X.ftok);  // entry of x under p: same key, now c
+      Rc.ds = X.ds;
+      Rc.ftok = X.ftok;
+      Rc.parent = p;
+      C.w.tab()[hi] = hentry(C, c);
+      C.w.rec()[p].cxor ^= x ^ c;
+      d_set_eff(C, Rc.dpos, node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM));
       C.c_wr += 2;
     }
     if (log) {
@@ -666,7 +746,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       *log_n = li + 1;
     }
     dense_remove_1(C, x);
-    C.w.flags()[x] = 0;
+    C.w.rec()[x].nf = 0;
     C.w.freel()[C.nfree++] = x;
   }
   sync_state(C);
@@ -678,36 +758,33 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
                                             uint32_t r) {
   const uint32_t u = alloc_1(C, P.status);
   if (u == NIL) return NIL;
-  const uint32_t p = C.w.parent()[y];
-  const uint32_t ods = C.w.ds()[y];
-  C.w.id()[u] = C.next_id++;
-  C.w.parent()[u] = p;
-  C.w.ds()[u] = ods;
-  C.w.de()[u] = x;
-  C.w.roff()[u] = C.w.roff()[y];
-  C.w.ftok()[u] = C.w.ftok()[y];
-  C.w.flags()[u] = stateful ? F_SSM : 0u;
-  C.w.t()[u] = r;
-  C.w.nchild()[u] = 1;
-  C.w.cxor()[u] = y;
-  C.w.hval()[hash_index_1(C, hkey_of(p, C.w.ftok()[u]))] = u;  // same key, new child
-  C.w.ds()[y] = x;
-  const uint32_t ft = P.tok[C.w.roff()[y] + x];
-  C.w.ftok()[y] = ft;
-  C.w.parent()[y] = u;
-  hash_insert_1(C, hkey_of(u, ft), y);
-  C.w.cxor()[p] ^= y ^ u;
-  dense_add_1(C, u);
-  dense_set_eff_1(C, y);
+  const NodeRec Y = C.w.rec()[y];
+  const uint32_t hi = hash_index_1(C, Y.parent, Y.ftok);  // entry of y under its parent
+  NodeRec U;
+  U.parent = Y.parent; U.ftok = Y.ftok; U.ds = Y.ds; U.de = x;
+  U.id = C.next_id++; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
+  C.w.rec()[u] = U;
+  const uint32_t ro = C.w.roff()[y];
+  C.w.roff()[u] = ro;
+  C.w.tab()[hi] = hentry(C, u);  // same key (parent, first token), new child
+  const uint32_t ft = P.tok[(uint64_t)ro + x];
+  NodeRec& Ry = C.w.rec()[y];
+  Ry.parent = u;
+  Ry.ds = x;
+  Ry.ftok = ft;
+  hash_insert_1(C, u, ft, y);
+  C.w.rec()[Y.parent].cxor ^= y ^ u;
+  dense_add_1(C, u, r);
+  d_set_eff(C, Y.dpos, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
   C.c_wr += 2;
   return u;
 }
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
-  C.w.flags()[x] |= F_SSM;
-  C.w.t()[x] = r;
-  dense_set_eff_1(C, x);
-  dense_refresh_1(C, x);
+  NodeRec& R = C.w.rec()[x];
+  R.nf |= F_SSM << 24;
+  d_set_eff(C, R.dpos, node_eff(C.m, R.ds, R.de, true));
+  set_t_1(C, x, r);
   C.c_wr += 1;
 }
 
@@ -727,35 +804,38 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   const uint32_t L_in = q.input_len;
   const uint32_t n = q.input_len + q.output_len;
 
+  PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
   uint32_t v = 0, pos = 0, npath = 0, m = 0;
   uint32_t partial = NIL, hit = NIL, reuse = 0;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
+  uint32_t v_flags = 0, lin_bnd_flags = 0;
   uint64_t pinned_bytes = 0;
   for (;;) {
     if (pos == n) { m = n; break; }
     const uint32_t tk = __ldg(P.tok + off + pos);
     const uint32_t c = hash_find_warp(C, v, tk);
     if (c == NIL) { m = pos; break; }
-    const uint32_t ds = C.w.ds()[c], de = C.w.de()[c], fl = C.w.flags()[c];
-    const uint64_t ro = C.w.roff()[c];
-    const uint32_t len = de - ds;
+    const NodeRec R = C.w.rec()[c];
+    const uint32_t fl = R.nf >> 24;
+    const uint32_t len = R.de - R.ds;
     const uint32_t cmp = min(len, n - pos);
-    const uint32_t k = match_len(P.tok, ro + ds, off + pos, cmp);
+    const uint32_t k = match_len(P.tok, (uint64_t)C.w.roff()[c] + R.ds, off + pos, cmp);
     if (lane == 0) {
       C.w.path()[npath] = c;
-      C.w.flags()[c] = fl | F_PIN;   // pin the path (R12)
-      C.w.dense()[C.w.dpos()[c]].tc |= NOTC;
+      C.w.rec()[c].nf = R.nf | (F_PIN << 24);   // pin the path (R12)
+      d_set_tc(C, R.dpos, d_tc(C, R.dpos) | NOTC);
     }
     npath++;
-    pinned_bytes += node_bytes(C.m, ds, de, fl & F_SSM);
+    pinned_bytes += node_bytes(C.m, R.ds, R.de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
     if (k == len) {
       v = c;
+      v_flags = fl;
       pos += len;
-      if (de == L_in) lin_bnd = c;
-      if ((fl & F_SSM) && de <= L_in) { hit = c; reuse = de; }  // all-or-nothing hit (R6, R7)
+      if (R.de == L_in) { lin_bnd = c; lin_bnd_flags = fl; }
+      if ((fl & F_SSM) && R.de <= L_in) { hit = c; reuse = R.de; }  // all-or-nothing hit (R6, R7)
     } else {
       m = pos + k;
       partial = c;
@@ -772,7 +852,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     hit = NIL;
     for (uint32_t i = 0; i < npath; i++) {
       const uint32_t x = C.w.path()[i];
-      if (C.w.ds()[x] < reuse) hit = x;
+      if (C.w.rec()[x].ds < reuse) hit = x;
     }
   }
 
@@ -782,7 +862,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   if (m_in > 0) {
     if (m >= L_in) {
       if (lin_bnd != NIL) {
-        if (!(C.w.flags()[lin_bnd] & F_SSM)) { p = m_in; p_gain = lin_bnd; }
+        if (!(lin_bnd_flags & F_SSM)) { p = m_in; p_gain = lin_bnd; }
       } else {
         p = m_in;
         p_split = lin_node;
@@ -790,7 +870,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     } else if (partial != NIL) {
       p = m_in;
       p_split = partial;
-    } else if (!(C.w.flags()[v] & F_SSM)) {
+    } else if (!(v_flags & F_SSM)) {
       p = m_in;
       p_gain = v;
     }
@@ -800,7 +880,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   const bool split_m = partial != NIL && m < n && m != p;   // stateless output-region split (R10)
   const bool split_n = partial != NIL && m == n && n != p;  // sequence ends inside an edge
   uint32_t n_gain = NIL;
-  if (partial == NIL && m == n && n != p && !(C.w.flags()[v] & F_SSM)) n_gain = v;
+  if (partial == NIL && m == n && n != p && !(v_flags & F_SSM)) n_gain = v;
   uint32_t n_ck = p ? 1u : 0u;
   if (n != p && (leaf || split_n || n_gain != NIL)) n_ck++;
   const uint64_t d_bytes = C.m.kvt * (uint64_t)(n - m) + C.m.ssmb * n_ck;
@@ -808,13 +888,11 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
 
   // Step 5: touch only the hit node.
   if (hit != NIL) {
-    if (lane == 0) {
-      C.w.t()[hit] = r;
-      dense_refresh_1(C, hit);
-    }
+    if (lane == 0) set_t_1(C, hit, r);
     C.c_wr += 1;
   }
   __syncwarp();
+  PHASE_MARK(C.t_walk);
 
   // Step 6: admission precheck (R12).
   const bool bypass = (pinned_bytes + d_bytes > C.capb) || (C.capn && npath + d_nodes > C.capn);
@@ -822,6 +900,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     // Step 7: evict the argmin utility until the request fits.
     while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + d_nodes > C.capn)))
       evict_one(C, P, r, log, log_n);
+    PHASE_MARK(C.t_evict);
     // Step 8: insert.
     if (lane == 0 && !C.failed) {
       uint32_t attach = v;  // node at depth m after the splits
@@ -836,28 +915,23 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
       if (leaf && !C.failed) {
         const uint32_t w = alloc_1(C, P.status);
         if (w != NIL) {
-          C.w.id()[w] = C.next_id++;
-          C.w.parent()[w] = attach;
-          C.w.ds()[w] = m;
-          C.w.de()[w] = n;
-          C.w.roff()[w] = off;
           const uint32_t ft = P.tok[off + m];
-          C.w.ftok()[w] = ft;
-          C.w.flags()[w] = F_SSM;
-          C.w.t()[w] = r;
-          C.w.nchild()[w] = 0;
-          C.w.cxor()[w] = 0;
-          hash_insert_1(C, hkey_of(attach, ft), w);
-          C.w.nchild()[attach] += 1;
-          C.w.cxor()[attach] ^= w;
-          if (attach != 0) dense_refresh_1(C, attach);
-          dense_add_1(C, w);
+          NodeRec W;
+          W.parent = attach; W.ftok = ft; W.ds = m; W.de = n;
+          W.id = C.next_id++; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
+          C.w.rec()[w] = W;
+          C.w.roff()[w] = (uint32_t)off;
+          hash_insert_1(C, attach, ft, w);
+          NodeRec& Ra = C.w.rec()[attach];
+          Ra.nf += 1;
+          Ra.cxor ^= w;
+          if (attach != 0) refresh_1(C, attach);
+          dense_add_1(C, w, r);
           C.c_wr += 1;
         }
       } else if (partial == NIL) {
         // final node at n already exists: timestamp it (R5)
-        C.w.t()[v] = r;
-        dense_refresh_1(C, v);
+        set_t_1(C, v, r);
         if (n_gain == NIL && p_gain != v) C.c_wr += 1;
       }
       C.total += d_bytes;
@@ -868,12 +942,13 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     }
     sync_state(C);
   }
+  PHASE_MARK(C.t_insert);
   // Step 9: unpin, outputs.
   if (lane == 0) {
     for (uint32_t i = 0; i < npath; i++) {
       const uint32_t x = C.w.path()[i];
-      C.w.flags()[x] &= ~F_PIN;
-      dense_refresh_1(C, x);
+      C.w.rec()[x].nf &= ~(F_PIN << 24);
+      refresh_1(C, x);
     }
     if (reuse > L_in) {
       atomicOr(P.status, ST_INVARIANT);
@@ -881,6 +956,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     }
   }
   sync_state(C);
+  PHASE_MARK(C.t_unpin);
   ReqOut o;
   o.reuse = reuse;
   o.flops = prefill_F(C.m, reuse);
@@ -889,15 +965,24 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
 }
 
 __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t worker, const DevVariant& V,
-                                           double alpha) {
-  C.w = ws_slice(P.ws + (uint64_t)worker * P.ws_stride, P.ncap, P.hcap);
+                                           double alpha, char* smem_warp, uint32_t S) {
+  C.w.b = P.ws + (uint64_t)worker * P.ws_stride;
+  C.w.n = P.ncap;
+  C.w.h = P.hcap;
+  C.seff = (double*)smem_warp;
+  C.stc = (uint32_t*)(smem_warp + 8ull * S);
+  C.S = S;
   C.ncap = P.ncap;
   C.hmask = P.hcap - 1;
+  C.gen = 0;
   C.m = V.m;
   C.capb = V.cap_bytes;
   C.capn = V.cap_nodes;
   C.alpha = alpha;
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
+#if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
+  C.t_walk = C.t_evict = C.t_insert = C.t_unpin = 0;
+#endif
   C.failed = false;
 }
 

@@ -49,7 +49,7 @@ class mc_replay_args(C.Structure):
                 ("d_hit", C.c_void_p), ("d_flops", C.c_void_p), ("d_bypass", C.c_void_p),
                 ("d_hit_sum", C.c_void_p), ("d_counters", C.c_void_p), ("d_log", C.c_void_p),
                 ("log_cap", C.c_uint32), ("d_log_n", C.c_void_p), ("d_chain_ns", C.c_void_p),
-                ("n_workers", C.c_uint32)]
+                ("n_workers", C.c_uint32), ("smem_nodes", C.c_uint32)]
 
 
 class MarconiError(RuntimeError):
@@ -215,7 +215,8 @@ class Context:
 
     def alloc_workspace(self, n_workers: int = 0, n_alpha: int = 1, n_chains: int = 0):
         nbytes = self.workspace_size(n_workers, n_alpha, n_chains)
-        return self.torch.empty(nbytes, dtype=self.torch.uint8, device=self.device)
+        # zero-initialised once (include/marconi.h: child-index generation tags start at 0)
+        return self.torch.zeros(nbytes, dtype=self.torch.uint8, device=self.device)
 
     # ---- live pass ----
     def live_pass(self, window: int, workspace=None, stream=None):
@@ -243,7 +244,7 @@ class Context:
 
     # ---- replay ----
     def replay(self, alphas, chains=None, workspace=None, out=None, log_cap: int = 0, counters: bool = False,
-               chain_cycles: bool = False, n_workers: int = 0, stream=None):
+               chain_cycles: bool = False, n_workers: int = 0, smem_nodes: int = 0, stream=None):
         """Launch the α-grid replay (asynchronous).  Returns a dict of device tensors:
         hit int32[n_var, n_alpha, R], flops int64[...], bypass uint8[...], hit_sum int64[n_var, n_alpha]
         (+ counters int64[n_chains_total, 4], log, log_n, cycles when requested)."""
@@ -273,6 +274,7 @@ class Context:
         args.d_log_n = out["log_n"].data_ptr() if out.get("log_n") is not None else None
         args.d_chain_ns = out["cycles"].data_ptr() if out.get("cycles") is not None else None
         args.n_workers = n_workers
+        args.smem_nodes = smem_nodes
         self._last_args = (alph, ch, ws, args)
         check(lib().mc_replay(self.h, C.byref(args), _stream_ptr(stream)))
         return out

@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
 for f in build/variants/*.so; do
-  MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -1
+  PHASES3=1 MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -2
 done | tee gpurun_out/variants.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log

@@ -29,3 +29,12 @@ ctr = out["counters"].cpu().numpy()
 print(f"{os.path.basename(os.environ.get('MARCONI_LIB', 'default'))} cfg{cfg}: replay ms {np.median(ts[1:]):.2f} "
       f"(min {min(ts[1:]):.2f}) chains {len(g.chains)} chain-cycles median {np.median(cyc)/1e6:.2f}M max {cyc.max()/1e6:.2f}M "
       f"hitsum {int(out['hit_sum'].sum())}", flush=True)
+if os.environ.get("PHASES"):
+    tot = ctr.astype(np.float64).sum(0)
+    print("phase cycles share walk/evict/insert/unpin:", np.round(tot / tot.sum(), 3), "per request (M):",
+          np.round(tot / (len(g.chains) * w.window) / 1e3, 1), "k-cycles")
+if os.environ.get("PHASES3"):
+    tot = ctr.astype(np.float64).sum(0)
+    nreq = len(g.chains) * w.window
+    print("per request k-cycles: pass1 %.1f pass2 %.1f verify %.1f ; fallbacks per request %.4f" %
+          (tot[0] / nreq / 1e3, tot[1] / nreq / 1e3, tot[2] / nreq / 1e3, tot[3] / nreq))
