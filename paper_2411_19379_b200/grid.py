@@ -65,6 +65,29 @@ def select_alpha(alphas: Sequence[float], hit_sums: np.ndarray) -> List[float]:
     return res
 
 
+def gather_hit_sums(hs, world: int, group=None):
+    """Sum every rank's partial u64[n_variant, n_alpha] hit sums (one all-gather).
+
+    NCCL (NVLink/NVSwitch): all_gather_into_tensor on the device tensor.  gloo
+    (CPU tests): the list form.  Summation is in rank order on every rank, exact
+    in int64, so all ranks hold identical totals.
+    """
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return hs
+    if dist.get_backend(group) == "nccl":
+        g = torch.empty((world,) + tuple(hs.shape), dtype=hs.dtype, device=hs.device)
+        dist.all_gather_into_tensor(g, hs.contiguous(), group=group)
+        return g.sum(0)
+    parts = [torch.empty_like(hs) for _ in range(world)]
+    dist.all_gather(parts, hs.contiguous(), group=group)
+    tot = torch.zeros_like(hs)
+    for p in parts:
+        tot += p
+    return tot
+
+
 class AlphaGrid:
     """One rank's share of an α-grid replay over segment windows.
 
@@ -117,12 +140,6 @@ class AlphaGrid:
         return self.ctx.replay(self.alphas, chains=self.chains, workspace=self.workspace, out=out, **kw)
 
     def select(self, out) -> List[float]:
-        import torch
-        hs = out["hit_sum"]
-        if self.world > 1:
-            import torch.distributed as dist
-            g = torch.empty((self.world,) + tuple(hs.shape), dtype=hs.dtype, device=hs.device)
-            dist.all_gather_into_tensor(g, hs.contiguous(), group=self.group)
-            hs = g.sum(0)
+        hs = gather_hit_sums(out["hit_sum"], self.world, self.group)
         self.hit_sums = hs.cpu().numpy()
         return select_alpha(self.alphas, self.hit_sums)
