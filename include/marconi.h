@@ -115,7 +115,7 @@ mc_status mc_create(const mc_variant* h_variants, uint32_t n_variants, uint32_t 
 void mc_destroy(mc_ctx* ctx);
 
 /* Borrow the trace (device pointers).  Validated synchronously (input_len >= 1,
- * ranges inside the pool, n_reqs < 2^31). */
+ * ranges inside the pool, n_reqs < 2^30, n_tokens < 2^32). */
 mc_status mc_set_trace(mc_ctx* ctx, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
                        uint32_t n_reqs);
 

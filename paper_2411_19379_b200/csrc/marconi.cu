@@ -37,7 +37,7 @@ mc_status fail(mc_status s, const std::string& m) {
   } while (0)
 
 #ifndef MC_MINBLOCKS
-#define MC_MINBLOCKS 3
+#define MC_MINBLOCKS 4
 #endif
 constexpr int kWarpsPerCta = 4;
 }  // namespace
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const DevVariant V = P.var[v];
     const mc_segment seg = P.segs[s];
     Chain C;
-    chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 12ull * P.smem_nodes, P.smem_nodes);
+    chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes, P.smem_nodes);
     load_snapshot(C, P, &P.snap[v], seg.snapshot);
     mc_evict_rec* log = P.log ? P.log + (uint64_t)c * P.log_cap : nullptr;
     uint32_t* log_n = P.log ? P.log_n + c : nullptr;
@@ -300,15 +300,15 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
   {
     const int64_t per_cta = std::min<int64_t>(smem_optin, smem_sm / MC_MINBLOCKS - 1024);
     const int64_t per_warp = per_cta / kWarpsPerCta;
-    c->smem_nodes = (uint32_t)std::max<int64_t>(0, (per_warp / 12) & ~31ll);
+    c->smem_nodes = (uint32_t)std::max<int64_t>(0, (per_warp / 8) & ~31ll);
     c->smem_nodes = std::min<uint32_t>(c->smem_nodes, max_nodes);
-    c->smem_nodes_live = std::min<uint32_t>((uint32_t)((smem_optin / 12) & ~31), max_nodes);
+    c->smem_nodes_live = std::min<uint32_t>((uint32_t)((smem_optin / 8) & ~31), max_nodes);
   }
   cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaFuncSetAttribute(live_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   int bps = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel, 32 * kWarpsPerCta,
-                                                kWarpsPerCta * 12ull * c->smem_nodes);
+                                                kWarpsPerCta * 8ull * c->smem_nodes);
   c->blocks_per_sm = std::max(1, bps);
   c->ncap = max_nodes;
   c->hcap = 2 * max_nodes;
@@ -354,7 +354,7 @@ void mc_destroy(mc_ctx* c) {
 mc_status mc_set_trace(mc_ctx* c, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
                        uint32_t n_reqs) {
   if (!c || !d_tokens || !d_reqs || n_reqs == 0) return fail(MC_EINVAL, "mc_set_trace: null/empty argument");
-  if (n_reqs >= (1u << 31)) return fail(MC_EINVAL, "too many requests (timestamps must stay < 2^31)");
+  if (n_reqs >= (1u << 30)) return fail(MC_EINVAL, "too many requests (timestamps must stay < 2^30)");
   if (n_tokens > 0xFFFFFFFFull) return fail(MC_EINVAL, "token pool must hold < 2^32 tokens (u32 node offsets)");
   std::vector<mc_request> h(n_reqs);
   CU(cudaMemcpy(h.data(), d_reqs, sizeof(mc_request) * n_reqs, cudaMemcpyDeviceToHost));
@@ -514,7 +514,7 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
   P.live_out = d_outs;
   P.window = window;
   P.smem_nodes = c->smem_nodes_live;
-  live_kernel<<<nv, 32, 12ull * c->smem_nodes_live, st>>>(P);
+  live_kernel<<<nv, 32, 8ull * c->smem_nodes_live, st>>>(P);
   CU(cudaGetLastError());
   // the last snapshot offset entry (K) for completeness
   std::vector<uint64_t> offK(1, (uint64_t)K * c->ncap);
@@ -635,10 +635,10 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   P.status = c->d_status;
   uint32_t S = A->smem_nodes ? A->smem_nodes : c->smem_nodes;
   S = std::min<uint32_t>(S, c->ncap) & ~31u;
-  if (kWarpsPerCta * 12ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
+  if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
   P.smem_nodes = S;
   const uint32_t ctas = (workers + kWarpsPerCta - 1) / kWarpsPerCta;
-  replay_kernel<<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 12ull * S, st>>>(P);
+  replay_kernel<<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
   CU(cudaGetLastError());
   return MC_OK;
 }

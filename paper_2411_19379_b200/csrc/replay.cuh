@@ -4,7 +4,7 @@
 // tree replayed request by request.
 //
 // Data layout per chain:
-//   shared memory  dense live-node list: t_last|NOTC (u32) and FLOP efficiency
+//   shared memory  dense live-node list: t_last|pin|multi (u32) and RN32(FLOP efficiency)
 //                  (f64) for positions < S -- the data every eviction scans;
 //   global (L2)    32-byte AoS node records {parent, first token, d_start, d_end |
 //                  id, child xor, nchild|flags, dense position}, u32 pool offsets,
@@ -34,8 +34,13 @@
 namespace mcd {
 
 constexpr uint32_t NIL = 0xFFFFFFFFu;
-constexpr uint32_t NOTC = 0x80000000u;  // dense tc: not an eviction candidate
-constexpr uint32_t F_SSM = 1u, F_PIN = 2u;  // node flags (bits 24.. of NodeRec::nf)
+// dense word tc = t_last (bits 0..29) | D_PIN | D_MULTI; a node is an eviction
+// candidate iff neither flag is set (<= 1 child and not on the current path)
+constexpr uint32_t D_PIN = 0x80000000u;    // on the current request's path (pinned, R12)
+constexpr uint32_t D_MULTI = 0x40000000u;  // >= 2 children
+constexpr uint32_t D_FLAGS = D_PIN | D_MULTI;
+constexpr uint32_t T_MASK = 0x3FFFFFFFu;
+constexpr uint32_t F_SSM = 1u;  // node flag (bits 24.. of NodeRec::nf)
 constexpr uint32_t NCH_MASK = 0x00FFFFFFu;
 constexpr uint32_t SLOT_BITS = 20, SLOT_MASK = (1u << SLOT_BITS) - 1, GEN_MAX = 4095;
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -80,15 +85,14 @@ struct DevSnapOut {
   uint32_t count, pad;
 };
 
-struct __align__(16) DenseRec {  // global tail of the dense list (positions >= S)
-  uint32_t tc;  // t_last | NOTC
-  uint32_t pad;
-  double eff;
+struct __align__(8) DenseRec {  // one dense position: the scanned key pair
+  uint32_t tc;  // t_last | D_PIN | D_MULTI
+  float e32;    // RN32(eff) -- filter and bounds; the exact eff lives in WS::eff64
 };
 
 struct __align__(16) NodeRec {
-  uint32_t parent, ftok, ds, de;  // first 16 B: what the walk and the child index read
-  uint32_t id, cxor, nf, dpos;    // nf = nchild (bits 0..23) | flags << 24
+  uint32_t parent, ftok, ds, de;  // first 16 B: what the child index reads
+  uint32_t roff, cxor, nf, dpos;  // roff = pool offset of the node's request; nf = nchild | flags << 24
 };
 
 struct KParams {
@@ -127,10 +131,11 @@ struct KParams {
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
   uint64_t b = 256                  // header
                + 32ull * ncap       // node records
-               + 4ull * ncap        // roff (u32)
+               + 4ull * ncap        // node ids
                + 4ull * hcap        // child index
                + 12ull * ncap       // dslot, path, freel
-               + 16ull * ncap;      // dense tail
+               + 8ull * ncap        // dense tail (positions >= S)
+               + 8ull * ncap;       // exact eff (f64) per dense position
   return (b + 255) & ~255ull;
 }
 
@@ -139,12 +144,13 @@ struct WS {
   uint32_t n, h;
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
-  __device__ __forceinline__ uint32_t* roff() const { return (uint32_t*)(b + 256 + 32ull * n); }
+  __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
   __device__ __forceinline__ uint32_t* tab() const { return (uint32_t*)(b + 256 + 36ull * n); }
   __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n + 4ull * h); }
   __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n + 4ull * h); }
   __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n + 4ull * h); }
   __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 48ull * n + 4ull * h); }
+  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 56ull * n + 4ull * h); }
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -158,7 +164,8 @@ __device__ __forceinline__ uint64_t prefill_F(const DevModel& m, uint64_t L) {
 __device__ __forceinline__ uint64_t node_bytes(const DevModel& m, uint32_t ds, uint32_t de, bool ssm) {
   return m.kvt * (uint64_t)(de - ds) + (ssm ? m.ssmb : 0ull);
 }
-__device__ __forceinline__ double node_eff(const DevModel& m, uint32_t ds, uint32_t de, bool ssm) {
+// out of line: the IEEE division sequence is long and the call sites are cold (I-cache)
+__device__ __forceinline__ double node_eff(DevModel m, uint32_t ds, uint32_t de, bool ssm) {
   uint64_t saved = prefill_F(m, de) - prefill_F(m, ds);  // relative to the parent
   return __ddiv_rn((double)saved, (double)node_bytes(m, ds, de, ssm));
 }
@@ -193,7 +200,7 @@ __device__ __forceinline__ void bounds_reduce(Bounds& b) {
   }
 }
 // u = rec + α·effn, each operation rounded (no FMA); degenerate range -> 0.5 (R2).
-__device__ __forceinline__ double utility(const Bounds& b, uint32_t t, double e, double alpha) {
+__device__ __forceinline__ double utility(Bounds b, uint32_t t, double e, double alpha) {
   double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(t - b.tmin), (double)(b.tmax - b.tmin));
   double effn = (b.emax == b.emin) ? 0.5 : __ddiv_rn(__dsub_rn(e, b.emin), __dsub_rn(b.emax, b.emin));
   return __dadd_rn(rec, __dmul_rn(alpha, effn));
@@ -229,8 +236,7 @@ __device__ __forceinline__ void best_reduce(Best& b) {
 // ---------------------------------------------------------------------------
 struct Chain {
   WS w;
-  uint32_t* stc;    // SMEM: dense t_last|NOTC for positions < S
-  double* seff;     // SMEM: dense eff for positions < S
+  DenseRec* sd;     // SMEM: dense {t_last|D_PIN|D_MULTI, RN32(eff)} for positions < S
   uint32_t S;       // SMEM-resident dense positions (the tail lives in global)
   uint32_t ncap, hmask, gen;
   uint32_t count;     // live non-root nodes (= dense list length)
@@ -332,24 +338,23 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
 }
 
 // ---- dense live list: positions < S in shared memory, the tail in global ----
-__device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return i < C.S ? C.stc[i] : C.w.tail()[i].tc; }
-__device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return i < C.S ? C.seff[i] : C.w.tail()[i].eff; }
-__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.rec()[C.w.dslot()[i]].id; }
-__device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) {
-  if (i < C.S) C.stc[i] = v; else C.w.tail()[i].tc = v;
-}
+__device__ __forceinline__ DenseRec* d_ptr(const Chain& C, uint32_t i) { return i < C.S ? C.sd + i : C.w.tail() + i; }
+__device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return d_ptr(C, i)->tc; }
+__device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return C.w.eff64()[i]; }
+__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[C.w.dslot()[i]]; }
+__device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
 __device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
-  if (i < C.S) C.seff[i] = v; else C.w.tail()[i].eff = v;
+  C.w.eff64()[i] = v;
+  d_ptr(C, i)->e32 = __double2float_rn(v);
 }
-__device__ __forceinline__ bool is_cand(uint32_t nf) { return (nf & NCH_MASK) <= 1 && !((nf >> 24) & F_PIN); }
-// (re)write node s's dense tc with timestamp t (lane 0)
-__device__ __forceinline__ void set_t_1(Chain& C, uint32_t s, uint32_t t) {
-  const NodeRec& R = C.w.rec()[s];
-  d_set_tc(C, R.dpos, t | (is_cand(R.nf) ? 0u : NOTC));
+// (re)stamp dense position i with timestamp t, keeping its flags (lane 0)
+__device__ __forceinline__ void d_stamp(Chain& C, uint32_t i, uint32_t t) {
+  DenseRec* d = d_ptr(C, i);
+  d->tc = t | (d->tc & D_FLAGS);
 }
-__device__ __forceinline__ void refresh_1(Chain& C, uint32_t s) {
-  const NodeRec& R = C.w.rec()[s];
-  d_set_tc(C, R.dpos, (d_tc(C, R.dpos) & ~NOTC) | (is_cand(R.nf) ? 0u : NOTC));
+__device__ __forceinline__ void d_multi(Chain& C, uint32_t i, uint32_t nchild) {
+  DenseRec* d = d_ptr(C, i);
+  d->tc = (d->tc & ~D_MULTI) | (nchild >= 2 ? D_MULTI : 0u);
 }
 __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   const uint32_t i = C.count++;
@@ -357,18 +362,7 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   R.dpos = i;
   C.w.dslot()[i] = s;
   d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
-  d_set_tc(C, i, t | (is_cand(R.nf) ? 0u : NOTC));
-}
-__device__ __forceinline__ void dense_remove_1(Chain& C, uint32_t s) {
-  const uint32_t i = C.w.rec()[s].dpos;
-  const uint32_t last = --C.count;
-  if (i != last) {
-    d_set_tc(C, i, d_tc(C, last));
-    d_set_eff(C, i, d_eff(C, last));
-    const uint32_t s2 = C.w.dslot()[last];
-    C.w.dslot()[i] = s2;
-    C.w.rec()[s2].dpos = i;
-  }
+  d_set_tc(C, i, t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u));
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
   if (C.nfree) return C.w.freel()[--C.nfree];
@@ -420,7 +414,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   __syncwarp();
   if (lane == 0) {
     NodeRec z;
-    z.parent = NIL; z.ftok = 0; z.ds = 0; z.de = 0; z.id = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
+    z.parent = NIL; z.ftok = 0; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
     C.w.rec()[0] = z;
   }
   uint64_t bytes = 0;
@@ -435,12 +429,12 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     R.ftok = P.tok[r.ref_off + r.d_start];
     R.ds = r.d_start;
     R.de = r.d_end;
-    R.id = r.id;
+    R.roff = (uint32_t)r.ref_off;
     R.cxor = 0;
     R.nf = (r.has_ssm ? F_SSM : 0u) << 24;
     R.dpos = i;
     C.w.rec()[s] = R;
-    C.w.roff()[s] = (uint32_t)r.ref_off;
+    C.w.ids()[s] = r.id;
     C.w.dslot()[i] = s;
     bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
   }
@@ -462,7 +456,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
-    d_set_tc(C, i, nodes[i].t_last | (is_cand(R.nf) ? 0u : NOTC));
+    d_set_tc(C, i, nodes[i].t_last | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u));
     d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
   }
 #pragma unroll
@@ -494,12 +488,12 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
     const NodeRec R = C.w.rec()[s];
     const uint32_t p = R.parent;
     mc_snap_node r;
-    r.id = R.id;
-    r.parent_id = (p == 0) ? 0u : C.w.rec()[p].id;
-    r.ref_off = C.w.roff()[s];
+    r.id = C.w.ids()[s];
+    r.parent_id = (p == 0) ? 0u : C.w.ids()[p];
+    r.ref_off = R.roff;
     r.d_start = R.ds;
     r.d_end = R.de;
-    r.t_last = d_tc(C, i) & ~NOTC;
+    r.t_last = d_tc(C, i) & T_MASK;
     r.has_ssm = ((R.nf >> 24) & F_SSM) ? 1u : 0u;
     dst[i] = r;
     pdst[i] = (p == 0) ? NIL : C.w.rec()[p].dpos;
@@ -548,52 +542,87 @@ constexpr int kUnroll = MC_UNROLL;
 #define PHASE_MARK(ctr) do {} while (0)
 #endif
 
-// Visit every dense position i < cnt as f(i, tc, eff): shared-memory part first,
-// then the global tail; kUnroll independent loads in flight per lane.
+// Visit every dense position i < cnt as f(q, i, tc, e32), q = unroll slot (so callers can
+// keep kUnroll independent accumulator sets): shared-memory part first, then the global
+// tail.  Full blocks of 32*kUnroll positions run without bounds checks.
 template <class F>
-__device__ __forceinline__ void scan_dense(const Chain& C, uint32_t cnt, F&& f) {
+__device__ __forceinline__ void scan_block(const DenseRec* __restrict__ d, uint32_t lo, uint32_t hi, F&& f) {
   const uint32_t lane = lane_id();
-  const uint32_t ns = min(cnt, C.S);
-  for (uint32_t base = 0; base < ns; base += 32 * kUnroll) {
-    uint32_t tc[kUnroll];
-    double e[kUnroll];
+  uint32_t base = lo;
+  for (; base + 32 * kUnroll <= hi; base += 32 * kUnroll) {
+    DenseRec r[kUnroll];
 #pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < ns) { tc[q] = C.stc[i]; e[q] = C.seff[i]; }
-    }
+    for (int q = 0; q < kUnroll; q++) r[q] = d[base + 32 * q + lane];
 #pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < ns) f(i, tc[q], e[q]);
-    }
+    for (int q = 0; q < kUnroll; q++) f(q, base + 32 * q + lane, r[q].tc, r[q].e32);
   }
-  const DenseRec* __restrict__ dn = C.w.tail();
-  for (uint32_t base = ns; base < cnt; base += 32 * kUnroll) {
-    DenseRec d[kUnroll];
-#pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < cnt) d[q] = dn[i];
-    }
-#pragma unroll
-    for (int q = 0; q < kUnroll; q++) {
-      const uint32_t i = base + 32 * q + lane;
-      if (i < cnt) f(i, d[q].tc, d[q].eff);
+  for (; base < hi; base += 32) {
+    const uint32_t i = base + lane;
+    if (i < hi) {
+      const DenseRec r = d[i];
+      f(0, i, r.tc, r.e32);
     }
   }
 }
+// Visit every dense position i < cnt as f(q, i, tc, e32), q = unroll slot (callers keep
+// kUnroll independent accumulator sets): shared-memory part first, then the global tail.
+template <class F>
+__device__ __forceinline__ void scan_dense(const Chain& C, uint32_t cnt, F&& f) {
+  const uint32_t ns = min(cnt, C.S);
+  scan_block(C.sd, 0, ns, f);
+  if (cnt > ns) scan_block(C.w.tail(), ns, cnt, f);
+}
 
+// Cold paths of the victim selection, kept out of line (instruction cache).
+__device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const DenseRec* tail, const double* e64,
+                                                 uint32_t cnt, uint32_t S, float lo32, float hi32) {
+  const uint32_t lane = lane_id();
+  double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const float e = (i < S ? sd[i] : tail[i]).e32;
+    if (e == lo32) elo = fmin(elo, e64[i]);
+    if (e == hi32) ehi = fmax(ehi, e64[i]);
+  }
+  return make_double2(elo, ehi);
+}
+__device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* tail, const double* e64,
+                                          const uint32_t* dslot, const uint32_t* ids, uint32_t cnt, uint32_t S,
+                                          Bounds b, double alpha) {
+  const uint32_t lane = lane_id();
+  Best best;
+  best_init(best);
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint32_t tc = (i < S ? sd[i] : tail[i]).tc;
+    if (tc & D_FLAGS) continue;
+    const double u = utility(b, tc, e64[i], alpha);
+    const uint32_t id = ids[dslot[i]];
+    if (best.i == NIL || better(u, tc, id, best)) {
+      best.u = u; best.t = tc; best.id = id; best.i = i;
+    }
+  }
+  best_reduce(best);
+  return best;
+}
+
+// Exact victim selection over the dense live list (Eq. 2).
+//   α = 0: u = rec exactly and rec is strictly monotone in t, so the victim is the
+//          candidate with the smallest (t_last, id) -- one integer pass (LRU).
+//   α > 0: pass 1 -- exact t bounds and fp32 eff bounds (RN32 is monotone, so the exact
+//          fp64 extremes are among the entries whose fp32 value equals the fp32 extreme;
+//          pass 2 reads only those fp64 values).  Pass 2 -- fp32 filter key per candidate,
+//          best two per lane.  Verify -- exact IEEE utility of the entries within δ of
+//          the minimum key; near-ties -> exact full pass.
 __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b) {
+  const uint32_t lane = lane_id();
   Best best;
   best_init(best);
   bounds_init(b);
   if (C.alpha == 0.0) {
-    scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double) {
-      const uint32_t t = tc & ~NOTC;
+    scan_dense(C, cnt, [&](int, uint32_t i, uint32_t tc, float) {
+      const uint32_t t = tc & T_MASK;
       b.tmin = min(b.tmin, t);
       b.tmax = max(b.tmax, t);
-      if (!(tc & NOTC) && t <= best.t) {
+      if (!(tc & D_FLAGS) && t <= best.t) {
         if (t < best.t) {
           best.t = t; best.i = i; best.id = NIL;  // id fetched lazily on a t tie
         } else {
@@ -603,11 +632,23 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
         }
       }
     });
-    if (best.i != NIL && best.id == NIL) best.id = d_id(C, best.i);
+    // resolve ids only when lanes tie on the minimum t
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       b.tmin = min(b.tmin, __shfl_xor_sync(FULL, b.tmin, o));
       b.tmax = max(b.tmax, __shfl_xor_sync(FULL, b.tmax, o));
+    }
+    uint32_t tbest = best.t;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tbest = min(tbest, __shfl_xor_sync(FULL, tbest, o));
+    const unsigned tied = __ballot_sync(FULL, best.i != NIL && best.t == tbest);
+    if (tied == 0) return best;
+    if (__popc(tied) > 1) {
+      if (best.i != NIL && best.t == tbest && best.id == NIL) best.id = d_id(C, best.i);
+    }
+    if (best.t != tbest) { best.i = NIL; best.id = NIL; best.t = 0xFFFFFFFFu; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
       const uint32_t t = __shfl_xor_sync(FULL, best.t, o);
       const uint32_t id = __shfl_xor_sync(FULL, best.id, o);
       const uint32_t i = __shfl_xor_sync(FULL, best.i, o);
@@ -615,10 +656,8 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
         best.t = t; best.id = id; best.i = i;
       }
     }
-    if (best.i != NIL) {
-      const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
-      best.u = __dadd_rn(rec, __dmul_rn(0.0, 0.5));  // = rec (α·effn = +0)
-    }
+    const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
+    best.u = __dadd_rn(rec, __dmul_rn(0.0, 0.5));  // = rec (α·effn = +0)
     return best;
   }
 #ifdef MC_PHASE_TIMERS3
@@ -628,47 +667,111 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
 #else
 #define T3(ctr) do {} while (0)
 #endif
-  // pass 1: bounds over ALL non-root nodes (R1)
-  scan_dense(C, cnt, [&](uint32_t, uint32_t tc, double e) { bounds_add(b, tc & ~NOTC, e); });
-  bounds_reduce(b);
-  T3(t_walk);
-  // pass 2: approximate keys in fp32, best two per lane (branch-free).
-  //   k = (t - tmin) * RN(1/Δt) + (RN32(e) - RN32(emin)) * RN32(α/Δe)
-  //   |k - (u - const)| <= E = 2^-21 (1 + α (1 + emax/Δe)),
-  //   so the exact argmin has k <= kmin + δ with δ = 2^-19 (1 + α (1 + emax/Δe)).
-  const bool dt0 = b.tmax == b.tmin, de0 = b.emax == b.emin;
-  const double de64 = __dsub_rn(b.emax, b.emin);
-  const float idt = dt0 ? 0.0f : __frcp_rn((float)(b.tmax - b.tmin));
-  const float aide = de0 ? 0.0f : __double2float_rn(__ddiv_rn(C.alpha, de64));
-  const float emin32 = __double2float_rn(b.emin);
-  const float INF = __int_as_float(0x7F800000);
-  float k1 = INF, k2 = INF;
-  uint32_t i1 = NIL;
-  scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double e) {
-    const float k = (tc & NOTC) ? INF
-                                : __fmaf_rn(__fsub_rn(__double2float_rn(e), emin32), aide,
-                                            __fmul_rn(__uint2float_rn(tc - b.tmin), idt));
-    const bool lt1 = k < k1, lt2 = k < k2;
-    k2 = lt1 ? k1 : (lt2 ? k : k2);
-    i1 = lt1 ? i : i1;
-    k1 = lt1 ? k : k1;
+  // pass 1: exact t bounds, fp32 eff bounds over ALL non-root nodes (R1)
+  uint32_t tmn[kUnroll], tmx[kUnroll];
+  float lo[kUnroll], hi[kUnroll];
+#pragma unroll
+  for (int q = 0; q < kUnroll; q++) {
+    tmn[q] = 0xFFFFFFFFu; tmx[q] = 0; lo[q] = __int_as_float(0x7F800000); hi[q] = 0.0f;
+  }
+  scan_dense(C, cnt, [&](int q, uint32_t, uint32_t tc, float e) {
+    const uint32_t t = tc & T_MASK;
+    tmn[q] = min(tmn[q], t);
+    tmx[q] = max(tmx[q], t);
+    lo[q] = fminf(lo[q], e);
+    hi[q] = fmaxf(hi[q], e);
   });
+  uint32_t tmin = tmn[0], tmax = tmx[0];
+  float lo32 = lo[0], hi32 = hi[0];
+#pragma unroll
+  for (int q = 1; q < kUnroll; q++) {
+    tmin = min(tmin, tmn[q]); tmax = max(tmax, tmx[q]); lo32 = fminf(lo32, lo[q]); hi32 = fmaxf(hi32, hi[q]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    tmin = min(tmin, __shfl_xor_sync(FULL, tmin, o));
+    tmax = max(tmax, __shfl_xor_sync(FULL, tmax, o));
+    lo32 = fminf(lo32, __shfl_xor_sync(FULL, lo32, o));
+    hi32 = fmaxf(hi32, __shfl_xor_sync(FULL, hi32, o));
+  }
+  b.tmin = tmin;
+  b.tmax = tmax;
+  T3(t_walk);
+  // pass 2: fp32 filter keys, best two per lane (branch-free), exact fp64 extremes
+  const bool dt0 = tmax == tmin;
+  const double de32 = (double)hi32 - (double)lo32;  // exact in fp64
+  const float idt = dt0 ? 0.0f : __frcp_rn((float)(tmax - tmin));
+  const float aide = (de32 == 0.0) ? 0.0f : __double2float_rn(__ddiv_rn(C.alpha, de32));
+  const float INF = __int_as_float(0x7F800000);
+  const double* __restrict__ e64 = C.w.eff64();
+  float a1[kUnroll], a2[kUnroll];
+  uint32_t ai[kUnroll];
+#pragma unroll
+  for (int q = 0; q < kUnroll; q++) { a1[q] = INF; a2[q] = INF; ai[q] = NIL; }
+  uint32_t ilo = NIL, ihi = NIL, nlo = 0, nhi = 0;
+  const float dmin = __uint2float_rn(tmin);
+  scan_dense(C, cnt, [&](int q, uint32_t i, uint32_t tc, float e) {
+    // entries holding the fp32 extremes (their fp64 values decide the exact bounds)
+    const bool el = e == lo32, eh = e == hi32;
+    ilo = el ? i : ilo;
+    nlo += el;
+    ihi = eh ? i : ihi;
+    nhi += eh;
+    const float k = (tc & D_FLAGS) ? INF : __fmaf_rn(__fsub_rn(e, lo32), aide, __fmul_rn(__uint2float_rn(tc - tmin), idt));
+    const bool lt1 = k < a1[q], lt2 = k < a2[q];
+    a2[q] = lt1 ? a1[q] : (lt2 ? k : a2[q]);
+    ai[q] = lt1 ? i : ai[q];
+    a1[q] = lt1 ? k : a1[q];
+  });
+  (void)dmin;
+  // merge the per-slot best-two lists
+  float k1 = a1[0], k2 = a2[0];
+  uint32_t i1 = ai[0];
+#pragma unroll
+  for (int q = 1; q < kUnroll; q++) {
+    if (a1[q] < k1) { k2 = fminf(k1, a2[q]); k1 = a1[q]; i1 = ai[q]; }
+    else { k2 = fminf(k2, a1[q]); }
+  }
+  // issue the fp64 reads this lane may need (extremes, its best candidate) before the
+  // warp reductions so their latency overlaps the shuffles
+  const double pre_lo = (nlo == 1) ? e64[ilo] : 0.0;
+  const double pre_hi = (nhi == 1) ? e64[ihi] : 0.0;
+  const double pre_k1 = (i1 != NIL) ? e64[i1] : 0.0;
+  double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
+  if (__any_sync(FULL, nlo > 1 || nhi > 1)) {
+    // several entries share an fp32 extreme: read all of their fp64 values (cold path)
+    const double2 ex = recover_extremes(C.sd, C.w.tail(), e64, cnt, C.S, lo32, hi32);
+    elo = ex.x;
+    ehi = ex.y;
+  } else {
+    if (nlo) elo = pre_lo;
+    if (nhi) ehi = pre_hi;
+  }
   float kmin = k1;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
+  for (int o = 16; o; o >>= 1) {
+    kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
+    elo = fmin(elo, __shfl_xor_sync(FULL, elo, o));
+    ehi = fmax(ehi, __shfl_xor_sync(FULL, ehi, o));
+  }
+  b.emin = elo;
+  b.emax = ehi;
   T3(t_evict);
   if (kmin == INF) return best;  // no candidate
-  const double ratio = de0 ? 0.0 : __ddiv_rn(b.emax, de64);
-  const double delta = 1.9073486328125e-06 * (1.0 + C.alpha * (1.0 + ratio));  // 2^-19 (1 + α (1 + emax/Δe))
+  // δ = 2^-19 (1 + α (1 + 4 emax/Δe32)); a zero fp32 range cannot resolve eff -> exact pass
+  const bool exact_only = (de32 == 0.0) && (b.emax != b.emin);
+  const double ratio = (de32 == 0.0) ? 0.0 : __ddiv_rn((double)hi32, de32);
+  const double delta = 1.9073486328125e-06 * (1.0 + C.alpha * (1.0 + 4.0 * ratio));
   const double lim = (double)kmin + delta;
-  if (!__any_sync(FULL, (double)k2 <= lim)) {
-    if ((double)k1 <= lim) {
-      const uint32_t tc = d_tc(C, i1);
-      best.u = utility(b, tc, d_eff(C, i1), C.alpha);
-      best.t = tc;
-      best.id = d_id(C, i1);
+  if (!exact_only && !__any_sync(FULL, (double)k2 <= lim)) {
+    const bool mine = (double)k1 <= lim;
+    if (mine) {
+      best.t = d_tc(C, i1);
+      best.u = utility(b, best.t, pre_k1, C.alpha);
       best.i = i1;
     }
+    const unsigned who = __ballot_sync(FULL, mine);
+    if (__popc(who) > 1 && mine) best.id = d_id(C, i1);  // ids only matter for exact ties
     best_reduce(best);
     T3(t_insert);
     return best;
@@ -676,30 +779,15 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
 #ifdef MC_PHASE_TIMERS3
   CC.t_unpin += 1;  // number of exact fallback passes
 #endif
-  // near-ties: exact full pass
-  scan_dense(C, cnt, [&](uint32_t i, uint32_t tc, double e) {
-    if (tc & NOTC) return;
-    const double u = utility(b, tc, e, C.alpha);
-    const uint32_t id = d_id(C, i);
-    if (best.i == NIL || better(u, tc, id, best)) {
-      best.u = u; best.t = tc; best.id = id; best.i = i;
-    }
-  });
-  best_reduce(best);
-  return best;
+  // near-ties / unresolvable fp32 range: exact full pass (cold path)
+  return exact_select(C.sd, C.w.tail(), e64, C.w.dslot(), C.w.ids(), cnt, C.S, b, C.alpha);
 }
 
 __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
   const uint32_t cnt = C.count;
   Bounds b;
-#ifdef MC_PHASE_TIMERS2
-  long long _ts = clock64();
-#endif
   const Best best = select_victim(C, cnt, b);
-#ifdef MC_PHASE_TIMERS2
-  C.t_unpin += (unsigned long long)(clock64() - _ts);
-#endif
   C.c_scan += cnt;
   if (best.i == NIL) {
     if (lane == 0) atomicOr(P.status, ST_NOCAND);
@@ -707,45 +795,66 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     return;
   }
   if (lane == 0) {
+    // Loads first (independent ones back to back), then the stores: every store
+    // below targets fields no later load in this block reads.
+    const uint32_t last = cnt - 1;
+    const uint32_t sl = C.w.dslot()[last];      // node moved into the freed dense position
+    const double e_last = C.w.eff64()[last];
     const uint32_t x = C.w.dslot()[best.i];
     const NodeRec X = C.w.rec()[x];
     const uint32_t p = X.parent;
     const uint32_t xf = X.nf >> 24;
+    const NodeRec Rp = C.w.rec()[p];
+    const uint32_t xid = log ? C.w.ids()[x] : 0u;
     uint32_t kind;
+    double e_moved = e_last;
     if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
       kind = 0;
+      const uint32_t hx = hash_index_1(C, p, X.ftok);
       C.total -= node_bytes(C.m, X.ds, X.de, xf & F_SSM);
-      hash_erase_at_1(C, hash_index_1(C, p, X.ftok));
-      NodeRec& Rp = C.w.rec()[p];
-      Rp.nf -= 1;
-      Rp.cxor ^= x;
-      if (p != 0) refresh_1(C, p);
+      hash_erase_at_1(C, hx);
+      NodeRec& Wp = C.w.rec()[p];
+      Wp.nf = Rp.nf - 1;
+      Wp.cxor = Rp.cxor ^ x;
+      if (p != 0) d_multi(C, Rp.dpos, (Rp.nf & NCH_MASK) - 1);
       C.c_wr += 1;
     } else {  // one child: release the state, the child absorbs the KVs
       kind = 1;
       const uint32_t c = X.cxor;
-      NodeRec& Rc = C.w.rec()[c];
+      const NodeRec Rc = C.w.rec()[c];
+      const uint32_t hc = hash_index_1(C, x, Rc.ftok);  // entry of c under x (erased)
+      const uint32_t hx = hash_index_1(C, p, X.ftok);   // entry of x under p (now c's)
       if (xf & F_SSM) C.total -= C.m.ssmb;
-      hash_erase_at_1(C, hash_index_1(C, x, Rc.ftok));
-      const uint32_t hi = hash_index_1(C, p, X.ftok);  // entry of x under p: same key, now c
-      Rc.ds = X.ds;
-      Rc.ftok = X.ftok;
-      Rc.parent = p;
-      C.w.tab()[hi] = hentry(C, c);
-      C.w.rec()[p].cxor ^= x ^ c;
-      d_set_eff(C, Rc.dpos, node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM));
+      NodeRec& Wc = C.w.rec()[c];
+      Wc.ds = X.ds;          // c's key becomes (p, first token of x) -- same home as hx
+      Wc.ftok = X.ftok;
+      Wc.parent = p;
+      C.w.tab()[hx] = hentry(C, c);
+      hash_erase_at_1(C, hc);
+      C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
+      const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
+      d_set_eff(C, Rc.dpos, ec);
+      if (Rc.dpos == last) e_moved = ec;
       C.c_wr += 2;
     }
     if (log) {
       const uint32_t li = *log_n;
       if (li < P.log_cap) {
         mc_evict_rec e;
-        e.req = r; e.node_id = best.id; e.kind = kind; e.n_live = cnt; e.utility = best.u;
+        e.req = r; e.node_id = xid; e.kind = kind; e.n_live = cnt; e.utility = best.u;
         log[li] = e;
       }
       *log_n = li + 1;
     }
-    dense_remove_1(C, x);
+    // dense_remove: move the last dense entry into the victim's position
+    const uint32_t i = X.dpos;
+    if (i != last) {
+      *d_ptr(C, i) = *d_ptr(C, last);
+      C.w.eff64()[i] = e_moved;
+      C.w.dslot()[i] = sl;
+      C.w.rec()[sl].dpos = i;
+    }
+    C.count = last;
     C.w.rec()[x].nf = 0;
     C.w.freel()[C.nfree++] = x;
   }
@@ -759,21 +868,21 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   const uint32_t u = alloc_1(C, P.status);
   if (u == NIL) return NIL;
   const NodeRec Y = C.w.rec()[y];
+  const uint32_t cx = C.w.rec()[Y.parent].cxor;
+  const uint32_t ft = P.tok[(uint64_t)Y.roff + x];
   const uint32_t hi = hash_index_1(C, Y.parent, Y.ftok);  // entry of y under its parent
   NodeRec U;
   U.parent = Y.parent; U.ftok = Y.ftok; U.ds = Y.ds; U.de = x;
-  U.id = C.next_id++; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
+  U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
   C.w.rec()[u] = U;
-  const uint32_t ro = C.w.roff()[y];
-  C.w.roff()[u] = ro;
+  C.w.ids()[u] = C.next_id++;
   C.w.tab()[hi] = hentry(C, u);  // same key (parent, first token), new child
-  const uint32_t ft = P.tok[(uint64_t)ro + x];
   NodeRec& Ry = C.w.rec()[y];
   Ry.parent = u;
   Ry.ds = x;
   Ry.ftok = ft;
   hash_insert_1(C, u, ft, y);
-  C.w.rec()[Y.parent].cxor ^= y ^ u;
+  C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
   d_set_eff(C, Y.dpos, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
   C.c_wr += 2;
@@ -782,20 +891,27 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   NodeRec& R = C.w.rec()[x];
-  R.nf |= F_SSM << 24;
-  d_set_eff(C, R.dpos, node_eff(C.m, R.ds, R.de, true));
-  set_t_1(C, x, r);
+  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de;
+  R.nf = nf | (F_SSM << 24);
+  d_set_eff(C, dp, node_eff(C.m, ds, de, true));
+  d_stamp(C, dp, r);
   C.c_wr += 1;
 }
 
 // ---------------------------------------------------------------------------
 // One request: SURVEY.md §8(c) c.2 steps 1-9.
+// The path P is held lane-distributed: lane i keeps path node i (i < 32), deeper
+// nodes spill to the workspace path array.
 // ---------------------------------------------------------------------------
 struct ReqOut {
   uint32_t reuse;
   uint64_t flops;
   bool bypass;
 };
+
+__device__ __forceinline__ uint32_t path_at(const Chain& C, uint32_t my_path, uint32_t i) {
+  return i < 32 ? __shfl_sync(FULL, my_path, i) : C.w.path()[i];
+}
 
 __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
@@ -806,27 +922,29 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
-  uint32_t v = 0, pos = 0, npath = 0, m = 0;
-  uint32_t partial = NIL, hit = NIL, reuse = 0;
+  uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL;
+  uint32_t partial = NIL, hit = NIL, reuse = 0, hit_dpos = NIL;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
-  uint32_t v_flags = 0, lin_bnd_flags = 0;
+  uint32_t v_flags = 0, lin_bnd_flags = 0, v_dpos = NIL;
   uint64_t pinned_bytes = 0;
+  uint32_t tk = __ldg(P.tok + off);
   for (;;) {
     if (pos == n) { m = n; break; }
-    const uint32_t tk = __ldg(P.tok + off + pos);
     const uint32_t c = hash_find_warp(C, v, tk);
     if (c == NIL) { m = pos; break; }
     const NodeRec R = C.w.rec()[c];
     const uint32_t fl = R.nf >> 24;
     const uint32_t len = R.de - R.ds;
+    // prefetch the query token the next level will look up
+    const uint32_t nt = (pos + len < n) ? __ldg(P.tok + off + pos + len) : 0u;
     const uint32_t cmp = min(len, n - pos);
-    const uint32_t k = match_len(P.tok, (uint64_t)C.w.roff()[c] + R.ds, off + pos, cmp);
+    const uint32_t k = match_len(P.tok, (uint64_t)R.roff + R.ds, off + pos, cmp);
     if (lane == 0) {
-      C.w.path()[npath] = c;
-      C.w.rec()[c].nf = R.nf | (F_PIN << 24);   // pin the path (R12)
-      d_set_tc(C, R.dpos, d_tc(C, R.dpos) | NOTC);
+      d_set_tc(C, R.dpos, d_tc(C, R.dpos) | D_PIN);   // pin the path (R12)
+      if (npath >= 32) C.w.path()[npath] = c;
     }
+    if (lane == npath) my_path = c;
     npath++;
     pinned_bytes += node_bytes(C.m, R.ds, R.de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
@@ -834,8 +952,9 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
       v = c;
       v_flags = fl;
       pos += len;
+      tk = nt;
       if (R.de == L_in) { lin_bnd = c; lin_bnd_flags = fl; }
-      if ((fl & F_SSM) && R.de <= L_in) { hit = c; reuse = R.de; }  // all-or-nothing hit (R6, R7)
+      if ((fl & F_SSM) && R.de <= L_in) { hit = c; reuse = R.de; hit_dpos = R.dpos; }  // all-or-nothing (R6, R7)
     } else {
       m = pos + k;
       partial = c;
@@ -851,9 +970,10 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     reuse = min(m, L_in);
     hit = NIL;
     for (uint32_t i = 0; i < npath; i++) {
-      const uint32_t x = C.w.path()[i];
+      const uint32_t x = path_at(C, my_path, i);
       if (C.w.rec()[x].ds < reuse) hit = x;
     }
+    hit_dpos = (hit != NIL) ? C.w.rec()[hit].dpos : NIL;
   }
 
   // Step 3: speculative insertion of the input (R8, R9).
@@ -888,7 +1008,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
 
   // Step 5: touch only the hit node.
   if (hit != NIL) {
-    if (lane == 0) set_t_1(C, hit, r);
+    if (lane == 0) d_stamp(C, hit_dpos, r);
     C.c_wr += 1;
   }
   __syncwarp();
@@ -916,22 +1036,23 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
         const uint32_t w = alloc_1(C, P.status);
         if (w != NIL) {
           const uint32_t ft = P.tok[off + m];
+          const NodeRec Ra = C.w.rec()[attach];
           NodeRec W;
           W.parent = attach; W.ftok = ft; W.ds = m; W.de = n;
-          W.id = C.next_id++; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
+          W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
           C.w.rec()[w] = W;
-          C.w.roff()[w] = (uint32_t)off;
+          C.w.ids()[w] = C.next_id++;
           hash_insert_1(C, attach, ft, w);
-          NodeRec& Ra = C.w.rec()[attach];
-          Ra.nf += 1;
-          Ra.cxor ^= w;
-          if (attach != 0) refresh_1(C, attach);
+          NodeRec& Wa = C.w.rec()[attach];
+          Wa.nf = Ra.nf + 1;
+          Wa.cxor = Ra.cxor ^ w;
+          if (attach != 0) d_multi(C, Ra.dpos, (Ra.nf & NCH_MASK) + 1);
           dense_add_1(C, w, r);
           C.c_wr += 1;
         }
       } else if (partial == NIL) {
         // final node at n already exists: timestamp it (R5)
-        set_t_1(C, v, r);
+        d_stamp(C, C.w.rec()[v].dpos, r);
         if (n_gain == NIL && p_gain != v) C.c_wr += 1;
       }
       C.total += d_bytes;
@@ -943,12 +1064,16 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
     sync_state(C);
   }
   PHASE_MARK(C.t_insert);
-  // Step 9: unpin, outputs.
+  // Step 9: unpin (every path lane clears its node's pin bit in parallel), outputs.
+  if (lane < min(npath, 32u)) {
+    const uint32_t dp = C.w.rec()[my_path].dpos;
+    DenseRec* d = d_ptr(C, dp);
+    d->tc &= ~D_PIN;
+  }
   if (lane == 0) {
-    for (uint32_t i = 0; i < npath; i++) {
-      const uint32_t x = C.w.path()[i];
-      C.w.rec()[x].nf &= ~(F_PIN << 24);
-      refresh_1(C, x);
+    for (uint32_t i = 32; i < npath; i++) {
+      DenseRec* d = d_ptr(C, C.w.rec()[C.w.path()[i]].dpos);
+      d->tc &= ~D_PIN;
     }
     if (reuse > L_in) {
       atomicOr(P.status, ST_INVARIANT);
@@ -969,8 +1094,7 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.w.b = P.ws + (uint64_t)worker * P.ws_stride;
   C.w.n = P.ncap;
   C.w.h = P.hcap;
-  C.seff = (double*)smem_warp;
-  C.stc = (uint32_t*)(smem_warp + 8ull * S);
+  C.sd = (DenseRec*)smem_warp;
   C.S = S;
   C.ncap = P.ncap;
   C.hmask = P.hcap - 1;

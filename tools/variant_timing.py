@@ -12,7 +12,7 @@ from paper_2411_19379_b200 import AlphaGrid
 
 cfg = int(os.environ.get("CFG", "3"))
 w = tg.workload(cfg)
-g = AlphaGrid(w.trace, w.variants, w.alphas, w.n_segments).setup()
+g = AlphaGrid(w.trace, w.variants, w.alphas, w.n_segments, max_nodes=int(os.environ.get('MAXN', '8192'))).setup()
 out = g.ctx.alloc_outputs(len(w.alphas), counters=True, chain_cycles=True)
 ts = []
 for it in range(6):
