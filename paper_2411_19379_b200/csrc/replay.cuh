@@ -926,7 +926,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   uint32_t partial = NIL, hit = NIL, reuse = 0, hit_dpos = NIL;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
-  uint32_t v_flags = 0, lin_bnd_flags = 0, v_dpos = NIL;
+  uint32_t v_flags = 0, lin_bnd_flags = 0;
   uint64_t pinned_bytes = 0;
   uint32_t tk = __ldg(P.tok + off);
   for (;;) {
