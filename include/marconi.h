@@ -107,7 +107,7 @@ typedef struct {
 typedef struct mc_ctx mc_ctx;
 
 /* Create a context for n_variants cache variants.  max_nodes (power of two,
- * 64 .. 2^20) sizes each chain's node table; exceeding it is MC_EOVERFLOW.
+ * 64 .. 16384) sizes each chain's node table; exceeding it is MC_EOVERFLOW.
  * Validation: bytes_per_param in {1,2,4}; n_attn >= 1 (a node without KVs and
  * without state would be zero bytes); d_model >= 1. */
 mc_status mc_create(const mc_variant* h_variants, uint32_t n_variants, uint32_t max_nodes, int device,

@@ -70,9 +70,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     if (lane == 0 && log_n) *log_n = 0;
     unsigned long long sum = 0;
     const uint64_t obase = ((uint64_t)v * P.n_alpha + a) * P.n_req;
+    Prefetched cur = fetch_request(P, seg.first_req), nxt = cur;
     for (uint32_t i = 0; i < seg.n_req && !C.failed; i++) {
       const uint32_t r = seg.first_req + i;
-      const ReqOut o = process_request(C, P, r, log, log_n);
+      const ReqOut o = process_request(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n);
+      cur = nxt;
       if (lane == 0) {
         P.hit[obase + r - 1] = o.reuse;
         P.flops[obase + r - 1] = o.flops;
@@ -111,8 +113,10 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
+  Prefetched cur = fetch_request(P, 1), nxt = cur;
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
-    const ReqOut o = process_request(C, P, r, nullptr, nullptr);
+    const ReqOut o = process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
+    cur = nxt;
     if (lane == 0) {
       const uint64_t k = (uint64_t)v * P.n_req + r - 1;
       if (P.hit) P.hit[k] = o.reuse;
@@ -272,8 +276,8 @@ const char* mc_last_error(void) { return g_err.c_str(); }
 mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, int device, mc_ctx** out) {
   if (!out || !hv || n_var == 0) return fail(MC_EINVAL, "mc_create: null argument or no variants");
   *out = nullptr;
-  if (max_nodes < 64 || max_nodes > (1u << 20) || (max_nodes & (max_nodes - 1)))
-    return fail(MC_EINVAL, "max_nodes must be a power of two in [64, 2^20]");
+  if (max_nodes < 64 || max_nodes > (1u << 14) || (max_nodes & (max_nodes - 1)))
+    return fail(MC_EINVAL, "max_nodes must be a power of two in [64, 16384] (14-bit slots in the child index)");
   for (uint32_t v = 0; v < n_var; v++) {
     const mc_model& m = hv[v].model;
     if (m.bytes_per_param != 1 && m.bytes_per_param != 2 && m.bytes_per_param != 4)

@@ -42,7 +42,10 @@ constexpr uint32_t D_FLAGS = D_PIN | D_MULTI;
 constexpr uint32_t T_MASK = 0x3FFFFFFFu;
 constexpr uint32_t F_SSM = 1u;  // node flag (bits 24.. of NodeRec::nf)
 constexpr uint32_t NCH_MASK = 0x00FFFFFFu;
-constexpr uint32_t SLOT_BITS = 20, SLOT_MASK = (1u << SLOT_BITS) - 1, GEN_MAX = 4095;
+// child-index entry (u64): first token (bits 0..31) | parent slot (32..45) |
+// child slot (46..59) | generation (60..63); an entry is live iff its generation is
+// the chain's, so the previous chain's entries are stale without clearing the table
+constexpr uint32_t GEN_MAX = 15, SLOT14 = 0x3FFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 // device status word bits (mc_check)
@@ -132,7 +135,7 @@ __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t 
   uint64_t b = 256                  // header
                + 32ull * ncap       // node records
                + 4ull * ncap        // node ids
-               + 4ull * hcap        // child index
+               + 8ull * hcap        // child index
                + 12ull * ncap       // dslot, path, freel
                + 8ull * ncap        // dense tail (positions >= S)
                + 8ull * ncap;       // exact eff (f64) per dense position
@@ -145,12 +148,12 @@ struct WS {
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
   __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
-  __device__ __forceinline__ uint32_t* tab() const { return (uint32_t*)(b + 256 + 36ull * n); }
-  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n + 4ull * h); }
-  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n + 4ull * h); }
-  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n + 4ull * h); }
-  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 48ull * n + 4ull * h); }
-  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 56ull * n + 4ull * h); }
+  __device__ __forceinline__ unsigned long long* tab() const { return (unsigned long long*)(b + 256 + 36ull * n); }
+  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n + 8ull * h); }
+  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n + 8ull * h); }
+  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n + 8ull * h); }
+  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 48ull * n + 8ull * h); }
+  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 56ull * n + 8ull * h); }
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -207,7 +210,7 @@ __device__ __forceinline__ double utility(Bounds b, uint32_t t, double e, double
 }
 struct Best {
   double u;
-  uint32_t t, id, i;
+  uint32_t t, id, i, slot;  // slot = dslot[i] when prefetched, else NIL
 };
 __device__ __forceinline__ bool better(double u, uint32_t t, uint32_t id, const Best& b) {
   return u < b.u || (u == b.u && (t < b.t || (t == b.t && id < b.id)));
@@ -217,6 +220,7 @@ __device__ __forceinline__ void best_init(Best& b) {
   b.t = 0xFFFFFFFFu;
   b.id = 0xFFFFFFFFu;
   b.i = NIL;
+  b.slot = NIL;
 }
 __device__ __forceinline__ void best_reduce(Best& b) {
 #pragma unroll
@@ -225,8 +229,9 @@ __device__ __forceinline__ void best_reduce(Best& b) {
     uint32_t t = __shfl_xor_sync(FULL, b.t, o);
     uint32_t id = __shfl_xor_sync(FULL, b.id, o);
     uint32_t i = __shfl_xor_sync(FULL, b.i, o);
+    uint32_t sl = __shfl_xor_sync(FULL, b.slot, o);
     if (i != NIL && (b.i == NIL || better(u, t, id, b))) {
-      b.u = u; b.t = t; b.id = id; b.i = i;
+      b.u = u; b.t = t; b.id = id; b.i = i; b.slot = sl;
     }
   }
 }
@@ -273,29 +278,32 @@ __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_
   key ^= key >> 33;
   return (uint32_t)key & mask;
 }
-__device__ __forceinline__ bool hvalid(const Chain& C, uint32_t e) { return (e >> SLOT_BITS) == C.gen; }
-__device__ __forceinline__ uint32_t hentry(const Chain& C, uint32_t slot) { return (C.gen << SLOT_BITS) | slot; }
+__device__ __forceinline__ bool hvalid(const Chain& C, unsigned long long e) { return (uint32_t)(e >> 60) == C.gen; }
+__device__ __forceinline__ unsigned long long hentry(const Chain& C, uint32_t parent, uint32_t tok, uint32_t slot) {
+  return ((unsigned long long)C.gen << 60) | ((unsigned long long)slot << 46) | ((unsigned long long)parent << 32) | tok;
+}
+__device__ __forceinline__ bool hmatch(unsigned long long e, uint32_t parent, uint32_t tok) {
+  return (uint32_t)e == tok && ((uint32_t)(e >> 32) & SLOT14) == parent;
+}
+__device__ __forceinline__ uint32_t hslot_of(unsigned long long e) { return (uint32_t)(e >> 46) & SLOT14; }
+__device__ __forceinline__ uint32_t hhome(const Chain& C, unsigned long long e) {
+  return hslot((uint32_t)(e >> 32) & SLOT14, (uint32_t)e, C.hmask);
+}
 
-// Warp-cooperative lookup of child(parent, tok): 32 probe positions per step; the
-// key of an entry is its node record's (parent, first token).
+// Warp-cooperative lookup of child(parent, tok): 32 probe positions per step, keys
+// compared in registers (no node-record reads).
 __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t parent, uint32_t tok) {
   const uint32_t h = hslot(parent, tok, C.hmask);
   const uint32_t lane = lane_id();
-  const uint32_t* __restrict__ tab = C.w.tab();
-  const NodeRec* __restrict__ rec = C.w.rec();
+  const unsigned long long* __restrict__ tab = C.w.tab();
   for (uint32_t base = 0; base <= C.hmask; base += 32) {
-    const uint32_t e = tab[(h + base + lane) & C.hmask];
+    const unsigned long long e = tab[(h + base + lane) & C.hmask];
     const bool valid = hvalid(C, e);
-    bool hit = false;
-    if (valid) {
-      const uint2 pf = *reinterpret_cast<const uint2*>(&rec[e & SLOT_MASK]);
-      hit = pf.x == parent && pf.y == tok;
-    }
-    const unsigned mm = __ballot_sync(FULL, hit);
+    const unsigned mm = __ballot_sync(FULL, valid && hmatch(e, parent, tok));
     const unsigned me = __ballot_sync(FULL, !valid);
     if (mm) {
       const int fm = __ffs(mm) - 1;
-      const uint32_t slot = __shfl_sync(FULL, e & SLOT_MASK, fm);
+      const uint32_t slot = __shfl_sync(FULL, hslot_of(e), fm);
       if (!me || fm < __ffs(me) - 1) return slot;
       return NIL;
     }
@@ -308,26 +316,24 @@ __device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t pare
 __device__ __forceinline__ uint32_t hash_index_1(const Chain& C, uint32_t parent, uint32_t tok) {
   uint32_t i = hslot(parent, tok, C.hmask);
   for (;;) {
-    const uint32_t e = C.w.tab()[i];
+    const unsigned long long e = C.w.tab()[i];
     if (!hvalid(C, e)) return NIL;
-    const NodeRec& R = C.w.rec()[e & SLOT_MASK];
-    if (R.parent == parent && R.ftok == tok) return i;
+    if (hmatch(e, parent, tok)) return i;
     i = (i + 1) & C.hmask;
   }
 }
 __device__ __forceinline__ void hash_insert_1(Chain& C, uint32_t parent, uint32_t tok, uint32_t slot) {
   uint32_t i = hslot(parent, tok, C.hmask);
   while (hvalid(C, C.w.tab()[i])) i = (i + 1) & C.hmask;
-  C.w.tab()[i] = hentry(C, slot);
+  C.w.tab()[i] = hentry(C, parent, tok, slot);
 }
 __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & C.hmask;
-    const uint32_t e = C.w.tab()[j];
+    const unsigned long long e = C.w.tab()[j];
     if (!hvalid(C, e)) break;
-    const NodeRec& R = C.w.rec()[e & SLOT_MASK];
-    const uint32_t home = hslot(R.parent, R.ftok, C.hmask);
+    const uint32_t home = hhome(C, e);
     const bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
     if (!stays) {
       C.w.tab()[i] = e;
@@ -447,9 +453,9 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     atomicXor(&C.w.rec()[ps].cxor, s);
     uint32_t j = hslot(ps, ft, C.hmask);
     for (;;) {
-      const uint32_t e = atomicAdd(&C.w.tab()[j], 0u);  // coherent read (other lanes insert concurrently)
+      const unsigned long long e = atomicAdd(&C.w.tab()[j], 0ull);  // coherent read (lanes insert concurrently)
       if (hvalid(C, e)) { j = (j + 1) & C.hmask; continue; }
-      if (atomicCAS(&C.w.tab()[j], e, hentry(C, s)) == e) break;
+      if (atomicCAS(&C.w.tab()[j], e, hentry(C, ps, ft, s)) == e) break;
     }
   }
   __syncwarp();
@@ -632,6 +638,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
         }
       }
     });
+    if (best.i != NIL) best.slot = C.w.dslot()[best.i];  // prefetch for the removal
     // resolve ids only when lanes tie on the minimum t
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -646,14 +653,15 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     if (__popc(tied) > 1) {
       if (best.i != NIL && best.t == tbest && best.id == NIL) best.id = d_id(C, best.i);
     }
-    if (best.t != tbest) { best.i = NIL; best.id = NIL; best.t = 0xFFFFFFFFu; }
+    if (best.t != tbest) { best.i = NIL; best.id = NIL; best.t = 0xFFFFFFFFu; best.slot = NIL; }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const uint32_t t = __shfl_xor_sync(FULL, best.t, o);
       const uint32_t id = __shfl_xor_sync(FULL, best.id, o);
       const uint32_t i = __shfl_xor_sync(FULL, best.i, o);
+      const uint32_t sl = __shfl_xor_sync(FULL, best.slot, o);
       if (i != NIL && (best.i == NIL || t < best.t || (t == best.t && id < best.id))) {
-        best.t = t; best.id = id; best.i = i;
+        best.t = t; best.id = id; best.i = i; best.slot = sl;
       }
     }
     const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
@@ -737,6 +745,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   const double pre_lo = (nlo == 1) ? e64[ilo] : 0.0;
   const double pre_hi = (nhi == 1) ? e64[ihi] : 0.0;
   const double pre_k1 = (i1 != NIL) ? e64[i1] : 0.0;
+  const uint32_t pre_slot = (i1 != NIL) ? C.w.dslot()[i1] : NIL;
   double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
   if (__any_sync(FULL, nlo > 1 || nhi > 1)) {
     // several entries share an fp32 extreme: read all of their fp64 values (cold path)
@@ -769,6 +778,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.t = d_tc(C, i1);
       best.u = utility(b, best.t, pre_k1, C.alpha);
       best.i = i1;
+      best.slot = pre_slot;
     }
     const unsigned who = __ballot_sync(FULL, mine);
     if (__popc(who) > 1 && mine) best.id = d_id(C, i1);  // ids only matter for exact ties
@@ -800,7 +810,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     const uint32_t last = cnt - 1;
     const uint32_t sl = C.w.dslot()[last];      // node moved into the freed dense position
     const double e_last = C.w.eff64()[last];
-    const uint32_t x = C.w.dslot()[best.i];
+    const uint32_t x = (best.slot != NIL) ? best.slot : C.w.dslot()[best.i];
     const NodeRec X = C.w.rec()[x];
     const uint32_t p = X.parent;
     const uint32_t xf = X.nf >> 24;
@@ -829,7 +839,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       Wc.ds = X.ds;          // c's key becomes (p, first token of x) -- same home as hx
       Wc.ftok = X.ftok;
       Wc.parent = p;
-      C.w.tab()[hx] = hentry(C, c);
+      C.w.tab()[hx] = hentry(C, p, X.ftok, c);
       hash_erase_at_1(C, hc);
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
       const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
@@ -876,7 +886,7 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
   C.w.rec()[u] = U;
   C.w.ids()[u] = C.next_id++;
-  C.w.tab()[hi] = hentry(C, u);  // same key (parent, first token), new child
+  C.w.tab()[hi] = hentry(C, Y.parent, Y.ftok, u);  // same key (parent, first token), new child
   NodeRec& Ry = C.w.rec()[y];
   Ry.parent = u;
   Ry.ds = x;
@@ -913,12 +923,29 @@ __device__ __forceinline__ uint32_t path_at(const Chain& C, uint32_t my_path, ui
   return i < 32 ? __shfl_sync(FULL, my_path, i) : C.w.path()[i];
 }
 
-__device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
+// Software pipelining across requests: the caller passes request r's header and
+// first token (loaded during request r-1); this request loads request r+1's header
+// at its start, its first token after the walk, and prefetches the child-index line
+// of its root lookup into L2 -- three dependent round trips off the critical path.
+struct Prefetched {
+  mc_request q;
+  uint32_t tk0;
+};
+__device__ __forceinline__ Prefetched fetch_request(const KParams& P, uint32_t r) {
+  Prefetched f;
+  f.q = P.req[r - 1];
+  f.tk0 = __ldg(P.tok + f.q.tok_off);
+  return f;
+}
+
+__device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const Prefetched cur, Prefetched& nxt,
+                                  bool has_next, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
-  const mc_request q = P.req[r - 1];
+  const mc_request q = cur.q;
   const uint64_t off = q.tok_off;
   const uint32_t L_in = q.input_len;
   const uint32_t n = q.input_len + q.output_len;
+  if (has_next) nxt.q = P.req[r];  // request r+1
 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
@@ -928,7 +955,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
   uint32_t v_flags = 0, lin_bnd_flags = 0;
   uint64_t pinned_bytes = 0;
-  uint32_t tk = __ldg(P.tok + off);
+  uint32_t tk = cur.tk0;
   for (;;) {
     if (pos == n) { m = n; break; }
     const uint32_t c = hash_find_warp(C, v, tk);
@@ -964,6 +991,13 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, mc_evi
   __syncwarp();
   C.c_cmp += min(m + 1, n);
   C.c_vis += npath + 1;
+  if (has_next) {
+    nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
+    if (lane == 0) {
+      const unsigned long long* line = C.w.tab() + hslot(0, nxt.tk0, C.hmask);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
+    }
+  }
 
   // Step 2: pure Transformer (n_ssm = 0): KVs can be sliced mid-edge.
   if (C.m.n_ssm == 0) {
