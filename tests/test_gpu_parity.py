@@ -26,6 +26,7 @@ DEV = torch.device("cuda", 0)
 
 def _assert_logs_equal(glog, gn, olog, ctx=""):
     assert gn == len(olog), (ctx, gn, len(olog))
+    olog = olog[: len(glog)]  # the device log keeps the first log_cap records
     assert np.array_equal(glog["req"], olog["req"]), ctx
     assert np.array_equal(glog["node_id"], olog["node_id"]), ctx
     assert np.array_equal(glog["kind"], olog["kind"]), ctx
@@ -276,36 +277,89 @@ def test_chain_subsets_and_order_do_not_matter():
         assert torch.equal(out[key], o2[key]), key
 
 
-def test_full_config3_sampled():
-    """BASELINE.json configs[2] at full size (50k requests, 16 α x 128 segments, the bench launch):
-    device snapshots and sampled chains vs the oracle; invariants on every chain."""
-    w = tg.workload(3)
+def _full_grid_parity(cfg, log_chains=()):
+    """All chains of BASELINE config `cfg` at full size, in the bench launch configuration,
+    against the oracle (live-pass snapshots, every request of every chain, hit sums, α*)."""
+    import os
+    w = tg.workload(cfg)
     tr = w.trace
     g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
-    out = g.run(counters=True)
+    out = g.run(counters=True, log_cap=16384 if log_chains else 0)
+    g.ctx.check()
+    hit, fl, by = (out[x].cpu().numpy() for x in ("hit", "flops", "bypass"))
+    ctr = out["counters"].cpu().numpy()
+    snaps, live, res, segs = GU.oracle_grid(tr, w.variants, w.alphas, w.n_segments, threads=os.cpu_count() or 1)
+    na, ns = len(w.alphas), len(segs)
+    for v in range(len(w.variants)):
+        lh = g.live[0].cpu().numpy()[v]
+        assert np.array_equal(lh, live[v][0]), v                      # device live pass == oracle live pass
+        for k in range(len(snaps[v])):
+            gs, gn = g.ctx.get_snapshot(v, k)
+            on, onid = snaps[v][k]
+            assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), (v, k)
+    for cid, (h, f, b, c) in res.items():
+        v, ai, si = cid // (na * ns), (cid // ns) % na, cid % ns
+        first, n, k = segs[si]
+        sl = slice(first - 1, first - 1 + n)
+        assert np.array_equal(hit[v, ai, sl], h), cid
+        assert np.array_equal(fl[v, ai, sl], f.astype(np.int64)), cid
+        assert np.array_equal(by[v, ai, sl], b.astype(np.uint8)), cid
+        assert np.array_equal(ctr[cid], c.astype(np.int64)), cid
+    for cid in log_chains:
+        v, ai, si = cid // (na * ns), (cid // ns) % na, cid % ns
+        first, n, k = segs[si]
+        _, _, _, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[v][k])
+        glog, gn = g.ctx.read_log(out, cid)
+        _assert_logs_equal(glog, gn, lg, f"cfg{cfg} chain {cid}")
+    a_star = g.select(out)
+    for v in range(len(w.variants)):
+        sums = [sum(int(res[(v * na + ai) * ns + si][0].sum()) for si in range(ns)) for ai in range(na)]
+        assert [int(x) for x in g.hit_sums[v]] == sums
+        assert a_star[v] == O.select_alpha(w.alphas, sums)
+    return g, out
+
+
+def test_full_config2_lmsys():
+    """configs[1]: LMSys-shaped 10k requests, one chain at α = 1 over the whole trace."""
+    _full_grid_parity(2, log_chains=(0,))
+
+
+def test_full_config3_sharegpt():
+    """configs[2] (the bench workload): 2,048 chains, every request, vs the oracle."""
+    _full_grid_parity(3, log_chains=(0, 127, 8 * 128 + 64, 15 * 128 + 127))
+
+
+def test_full_config4_swebench():
+    """configs[3]: SWEBench-shaped, contexts up to 32,768 tokens, 2,048 chains."""
+    _full_grid_parity(4, log_chains=(5, 9 * 128 + 77))
+
+
+def test_full_config5_sampled():
+    """configs[4]: 200k requests x 15 cache variants (1:2/1:4/1:8 x 60-140 GB) x 16 α x 16
+    segments = 3,840 chains on the device; sampled snapshots/chains vs the oracle, and
+    invariants on every chain."""
+    w = tg.workload(5)
+    tr = w.trace
+    g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
+    out = g.run()
     g.ctx.check()
     hit = out["hit"].cpu().numpy()
-    # invariants at full size: hit <= L_in; α = 0 segment replay == device live pass
+    live = g.live[0].cpu().numpy()
     assert (hit <= tr.lin[None, None, :]).all()
-    lh = g.live[0].cpu().numpy()[0]
-    assert np.array_equal(hit[0, 0], lh)
-    # sampled snapshots / chains against the oracle
+    for v in range(len(w.variants)):
+        assert np.array_equal(hit[v, 0], live[v])          # α = 0 segment replays == live pass
     W = g.window
-    sample_k = [1, 37, 127]
-    snaps, h_live, f_live, b_live = O.live_pass(tr, w.variants[0], W, upto=max(sample_k) * W)
-    assert np.array_equal(lh[: len(h_live)], h_live)
-    for k in sample_k:
-        gs, gn = g.ctx.get_snapshot(0, k)
-        on, onid = snaps[k]
-        assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), k
-    ns = len(g.segs)
-    for k in sample_k:
-        for ai in (0, 5, 8, 15):
-            first, n, _ = g.segs[k]
-            h, f, b, lg = GU.oracle_chain_log(tr, w.variants[0], w.alphas[ai], first, n, snaps[k])
-            assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h), (k, ai)
+    for v in (0, 7, 14):
+        snaps, h_live, *_ = O.live_pass(tr, w.variants[v], W, upto=2 * W)
+        assert np.array_equal(live[v][: 2 * W], h_live)
+        gs, gn = g.ctx.get_snapshot(v, 1)
+        assert gn == snaps[1][1] and np.array_equal(GU.canon(gs), GU.canon(snaps[1][0])), v
+        for ai in (1, 8, 15):
+            first, n, _ = g.segs[1]
+            h, f, b, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[1])
+            assert np.array_equal(hit[v, ai, first - 1:first - 1 + n], h), (v, ai)
     a_star = g.select(out)
-    assert a_star[0] in w.alphas
+    assert len(a_star) == 15 and all(a in w.alphas for a in a_star)
 
 
 def test_errors_are_loud():
