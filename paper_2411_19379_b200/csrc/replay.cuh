@@ -42,10 +42,14 @@ constexpr uint32_t D_FLAGS = D_PIN | D_MULTI;
 constexpr uint32_t T_MASK = 0x3FFFFFFFu;
 constexpr uint32_t F_SSM = 1u;  // node flag (bits 24.. of NodeRec::nf)
 constexpr uint32_t NCH_MASK = 0x00FFFFFFu;
-// child-index entry (u64): first token (bits 0..31) | parent slot (32..45) |
-// child slot (46..59) | generation (60..63); an entry is live iff its generation is
-// the chain's, so the previous chain's entries are stale without clearing the table
+// child-index entry (16 B): {first token, gen<<28 | parent slot<<14 | child slot,
+// d_end | has_ssm<<31, pool offset}.  An entry is live iff its generation is the
+// chain's (the previous chain's entries are stale without clearing the table); it
+// carries everything the walk needs about the child, so the walk reads no records.
 constexpr uint32_t GEN_MAX = 15, SLOT14 = 0x3FFFu;
+struct __align__(16) HEnt {
+  uint32_t tok, key, de, roff;
+};
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
 // device status word bits (mc_check)
@@ -134,8 +138,8 @@ struct KParams {
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
   uint64_t b = 256                  // header
                + 32ull * ncap       // node records
-               + 4ull * ncap        // node ids
-               + 8ull * hcap        // child index
+               + 16ull * ncap       // node ids (4 B, padded so the child index is 16 B aligned)
+               + 16ull * hcap       // child index
                + 12ull * ncap       // dslot, path, freel
                + 8ull * ncap        // dense tail (positions >= S)
                + 8ull * ncap;       // exact eff (f64) per dense position
@@ -147,13 +151,13 @@ struct WS {
   uint32_t n, h;
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
+  __device__ __forceinline__ HEnt* tab() const { return (HEnt*)(b + 256 + 48ull * n); }  // 16 B aligned
   __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
-  __device__ __forceinline__ unsigned long long* tab() const { return (unsigned long long*)(b + 256 + 36ull * n); }
-  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n + 8ull * h); }
-  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n + 8ull * h); }
-  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n + 8ull * h); }
-  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 48ull * n + 8ull * h); }
-  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 56ull * n + 8ull * h); }
+  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 48ull * n + 16ull * h); }
+  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 52ull * n + 16ull * h); }
+  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 56ull * n + 16ull * h); }
+  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 64ull * n + 16ull * h); }
+  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 72ull * n + 16ull * h); }
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -278,61 +282,75 @@ __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_
   key ^= key >> 33;
   return (uint32_t)key & mask;
 }
-__device__ __forceinline__ bool hvalid(const Chain& C, unsigned long long e) { return (uint32_t)(e >> 60) == C.gen; }
-__device__ __forceinline__ unsigned long long hentry(const Chain& C, uint32_t parent, uint32_t tok, uint32_t slot) {
-  return ((unsigned long long)C.gen << 60) | ((unsigned long long)slot << 46) | ((unsigned long long)parent << 32) | tok;
+__device__ __forceinline__ bool hvalid(const Chain& C, uint32_t key) { return (key >> 28) == C.gen; }
+__device__ __forceinline__ uint32_t hkey(const Chain& C, uint32_t parent, uint32_t slot) {
+  return (C.gen << 28) | (parent << 14) | slot;
 }
-__device__ __forceinline__ bool hmatch(unsigned long long e, uint32_t parent, uint32_t tok) {
-  return (uint32_t)e == tok && ((uint32_t)(e >> 32) & SLOT14) == parent;
+__device__ __forceinline__ HEnt hmake(const Chain& C, uint32_t parent, uint32_t tok, uint32_t slot, uint32_t de,
+                                      bool ssm, uint32_t roff) {
+  HEnt e;
+  e.tok = tok;
+  e.key = hkey(C, parent, slot);
+  e.de = de | (ssm ? 0x80000000u : 0u);
+  e.roff = roff;
+  return e;
 }
-__device__ __forceinline__ uint32_t hslot_of(unsigned long long e) { return (uint32_t)(e >> 46) & SLOT14; }
-__device__ __forceinline__ uint32_t hhome(const Chain& C, unsigned long long e) {
-  return hslot((uint32_t)(e >> 32) & SLOT14, (uint32_t)e, C.hmask);
+__device__ __forceinline__ bool hmatch(const HEnt& e, uint32_t parent, uint32_t tok) {
+  return e.tok == tok && ((e.key >> 14) & SLOT14) == parent;
+}
+__device__ __forceinline__ uint32_t hhome(const Chain& C, const HEnt& e) {
+  return hslot((e.key >> 14) & SLOT14, e.tok, C.hmask);
 }
 
 // Warp-cooperative lookup of child(parent, tok): 32 probe positions per step, keys
-// compared in registers (no node-record reads).
-__device__ __forceinline__ uint32_t hash_find_warp(const Chain& C, uint32_t parent, uint32_t tok) {
+// compared in registers.  Returns the entry (key == 0 when absent).
+__device__ __forceinline__ HEnt hash_find_warp(const Chain& C, uint32_t parent, uint32_t tok) {
   const uint32_t h = hslot(parent, tok, C.hmask);
   const uint32_t lane = lane_id();
-  const unsigned long long* __restrict__ tab = C.w.tab();
+  const HEnt* __restrict__ tab = C.w.tab();
+  HEnt none;
+  none.tok = 0; none.key = 0; none.de = 0; none.roff = 0;
   for (uint32_t base = 0; base <= C.hmask; base += 32) {
-    const unsigned long long e = tab[(h + base + lane) & C.hmask];
-    const bool valid = hvalid(C, e);
+    const HEnt e = tab[(h + base + lane) & C.hmask];
+    const bool valid = hvalid(C, e.key);
     const unsigned mm = __ballot_sync(FULL, valid && hmatch(e, parent, tok));
     const unsigned me = __ballot_sync(FULL, !valid);
     if (mm) {
       const int fm = __ffs(mm) - 1;
-      const uint32_t slot = __shfl_sync(FULL, hslot_of(e), fm);
-      if (!me || fm < __ffs(me) - 1) return slot;
-      return NIL;
+      HEnt r;
+      r.tok = tok;
+      r.key = __shfl_sync(FULL, e.key, fm);
+      r.de = __shfl_sync(FULL, e.de, fm);
+      r.roff = __shfl_sync(FULL, e.roff, fm);
+      if (!me || fm < __ffs(me) - 1) return r;
+      return none;
     }
-    if (me) return NIL;
+    if (me) return none;
   }
-  return NIL;
+  return none;
 }
 
 // ---- single-thread (lane 0) child-index mutations: linear probing, backward-shift delete ----
 __device__ __forceinline__ uint32_t hash_index_1(const Chain& C, uint32_t parent, uint32_t tok) {
   uint32_t i = hslot(parent, tok, C.hmask);
   for (;;) {
-    const unsigned long long e = C.w.tab()[i];
-    if (!hvalid(C, e)) return NIL;
+    const HEnt e = C.w.tab()[i];
+    if (!hvalid(C, e.key)) return NIL;
     if (hmatch(e, parent, tok)) return i;
     i = (i + 1) & C.hmask;
   }
 }
-__device__ __forceinline__ void hash_insert_1(Chain& C, uint32_t parent, uint32_t tok, uint32_t slot) {
-  uint32_t i = hslot(parent, tok, C.hmask);
-  while (hvalid(C, C.w.tab()[i])) i = (i + 1) & C.hmask;
-  C.w.tab()[i] = hentry(C, parent, tok, slot);
+__device__ __forceinline__ void hash_insert_1(Chain& C, const HEnt& ne, uint32_t parent) {
+  uint32_t i = hslot(parent, ne.tok, C.hmask);
+  while (hvalid(C, C.w.tab()[i].key)) i = (i + 1) & C.hmask;
+  C.w.tab()[i] = ne;
 }
 __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & C.hmask;
-    const unsigned long long e = C.w.tab()[j];
-    if (!hvalid(C, e)) break;
+    const HEnt e = C.w.tab()[j];
+    if (!hvalid(C, e.key)) break;
     const uint32_t home = hhome(C, e);
     const bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
     if (!stays) {
@@ -340,7 +358,7 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
       i = j;
     }
   }
-  C.w.tab()[i] = 0;
+  C.w.tab()[i].key = 0;
 }
 
 // ---- dense live list: positions < S in shared memory, the tail in global ----
@@ -415,7 +433,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   g = __shfl_sync(FULL, g, 0);
   clear = __shfl_sync(FULL, (int)clear, 0);
   if (clear)
-    for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.tab()[i] = 0;
+    for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.tab()[i].key = 0;
   C.gen = g;
   __syncwarp();
   if (lane == 0) {
@@ -452,11 +470,16 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     atomicAdd(&C.w.rec()[ps].nf, 1u);
     atomicXor(&C.w.rec()[ps].cxor, s);
     uint32_t j = hslot(ps, ft, C.hmask);
+    const uint32_t nk = hkey(C, ps, s);
     for (;;) {
-      const unsigned long long e = atomicAdd(&C.w.tab()[j], 0ull);  // coherent read (lanes insert concurrently)
-      if (hvalid(C, e)) { j = (j + 1) & C.hmask; continue; }
-      if (atomicCAS(&C.w.tab()[j], e, hentry(C, ps, ft, s)) == e) break;
+      const uint32_t k = atomicAdd(&C.w.tab()[j].key, 0u);  // coherent read (lanes insert concurrently)
+      if (hvalid(C, k)) { j = (j + 1) & C.hmask; continue; }
+      if (atomicCAS(&C.w.tab()[j].key, k, nk) == k) break;
     }
+    HEnt& E = C.w.tab()[j];
+    E.tok = ft;
+    E.de = R.de | (((R.nf >> 24) & F_SSM) ? 0x80000000u : 0u);
+    E.roff = R.roff;
   }
   __syncwarp();
   for (uint32_t i = lane; i < n; i += 32) {
@@ -781,7 +804,17 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.slot = pre_slot;
     }
     const unsigned who = __ballot_sync(FULL, mine);
-    if (__popc(who) > 1 && mine) best.id = d_id(C, i1);  // ids only matter for exact ties
+    if (__popc(who) == 1) {  // the common case: one candidate survives the filter
+      const int src = __ffs(who) - 1;
+      best.u = __shfl_sync(FULL, best.u, src);
+      best.t = __shfl_sync(FULL, best.t, src);
+      best.i = __shfl_sync(FULL, best.i, src);
+      best.slot = __shfl_sync(FULL, best.slot, src);
+      best.id = NIL;
+      T3(t_insert);
+      return best;
+    }
+    if (mine) best.id = d_id(C, i1);  // ids only matter for exact ties
     best_reduce(best);
     T3(t_insert);
     return best;
@@ -839,7 +872,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       Wc.ds = X.ds;          // c's key becomes (p, first token of x) -- same home as hx
       Wc.ftok = X.ftok;
       Wc.parent = p;
-      C.w.tab()[hx] = hentry(C, p, X.ftok, c);
+      C.w.tab()[hx] = hmake(C, p, X.ftok, c, Rc.de, (Rc.nf >> 24) & F_SSM, Rc.roff);
       hash_erase_at_1(C, hc);
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
       const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
@@ -886,12 +919,12 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
   C.w.rec()[u] = U;
   C.w.ids()[u] = C.next_id++;
-  C.w.tab()[hi] = hentry(C, Y.parent, Y.ftok, u);  // same key (parent, first token), new child
+  C.w.tab()[hi] = hmake(C, Y.parent, Y.ftok, u, x, stateful, Y.roff);  // same key, new child
   NodeRec& Ry = C.w.rec()[y];
   Ry.parent = u;
   Ry.ds = x;
   Ry.ftok = ft;
-  hash_insert_1(C, u, ft, y);
+  hash_insert_1(C, hmake(C, u, ft, y, Y.de, (Y.nf >> 24) & F_SSM, Y.roff), u);
   C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
   d_set_eff(C, Y.dpos, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
@@ -901,8 +934,10 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   NodeRec& R = C.w.rec()[x];
-  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de;
+  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de, pa = R.parent, ft = R.ftok;
+  const uint32_t hi = hash_index_1(C, pa, ft);
   R.nf = nf | (F_SSM << 24);
+  C.w.tab()[hi].de = de | 0x80000000u;  // the child index carries the state flag for the walk
   d_set_eff(C, dp, node_eff(C.m, ds, de, true));
   d_stamp(C, dp, r);
   C.c_wr += 1;
@@ -950,7 +985,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
   uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL;
-  uint32_t partial = NIL, hit = NIL, reuse = 0, hit_dpos = NIL;
+  uint32_t partial = NIL, hit = NIL, reuse = 0, hit_idx = NIL;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
   uint32_t v_flags = 0, lin_bnd_flags = 0;
@@ -958,30 +993,28 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   uint32_t tk = cur.tk0;
   for (;;) {
     if (pos == n) { m = n; break; }
-    const uint32_t c = hash_find_warp(C, v, tk);
-    if (c == NIL) { m = pos; break; }
-    const NodeRec R = C.w.rec()[c];
-    const uint32_t fl = R.nf >> 24;
-    const uint32_t len = R.de - R.ds;
+    const HEnt E = hash_find_warp(C, v, tk);  // one round trip per level: no record reads
+    if (E.key == 0) { m = pos; break; }
+    const uint32_t c = E.key & SLOT14;
+    const uint32_t de = E.de & 0x7FFFFFFFu;
+    const uint32_t fl = E.de >> 31;             // has_ssm
+    const uint32_t len = de - pos;              // the child's edge starts at the parent's depth
     // prefetch the query token the next level will look up
-    const uint32_t nt = (pos + len < n) ? __ldg(P.tok + off + pos + len) : 0u;
+    const uint32_t nt = (de < n) ? __ldg(P.tok + off + de) : 0u;
     const uint32_t cmp = min(len, n - pos);
-    const uint32_t k = match_len(P.tok, (uint64_t)R.roff + R.ds, off + pos, cmp);
-    if (lane == 0) {
-      d_set_tc(C, R.dpos, d_tc(C, R.dpos) | D_PIN);   // pin the path (R12)
-      if (npath >= 32) C.w.path()[npath] = c;
-    }
+    const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, off + pos, cmp);
+    if (lane == 0 && npath >= 32) C.w.path()[npath] = c;
     if (lane == npath) my_path = c;
     npath++;
-    pinned_bytes += node_bytes(C.m, R.ds, R.de, fl & F_SSM);
+    pinned_bytes += node_bytes(C.m, pos, de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
     if (k == len) {
       v = c;
       v_flags = fl;
       pos += len;
       tk = nt;
-      if (R.de == L_in) { lin_bnd = c; lin_bnd_flags = fl; }
-      if ((fl & F_SSM) && R.de <= L_in) { hit = c; reuse = R.de; hit_dpos = R.dpos; }  // all-or-nothing (R6, R7)
+      if (de == L_in) { lin_bnd = c; lin_bnd_flags = fl; }
+      if ((fl & F_SSM) && de <= L_in) { hit = c; reuse = de; hit_idx = npath - 1; }  // all-or-nothing (R6, R7)
     } else {
       m = pos + k;
       partial = c;
@@ -994,7 +1027,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   if (has_next) {
     nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
     if (lane == 0) {
-      const unsigned long long* line = C.w.tab() + hslot(0, nxt.tk0, C.hmask);
+      const HEnt* line = C.w.tab() + hslot(0, nxt.tk0, C.hmask);
       asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
     }
   }
@@ -1003,12 +1036,28 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   if (C.m.n_ssm == 0) {
     reuse = min(m, L_in);
     hit = NIL;
+    hit_idx = NIL;
     for (uint32_t i = 0; i < npath; i++) {
       const uint32_t x = path_at(C, my_path, i);
-      if (C.w.rec()[x].ds < reuse) hit = x;
+      if (C.w.rec()[x].ds < reuse) { hit = x; hit_idx = i; }
     }
-    hit_dpos = (hit != NIL) ? C.w.rec()[hit].dpos : NIL;
   }
+
+  // Pin the path (R12) and touch only the hit node (step 5): every path
+  // lane reads its node's dense position and updates its dense word in parallel.
+  if (lane < min(npath, 32u)) {
+    const uint32_t dp = C.w.rec()[my_path].dpos;
+    DenseRec* d = d_ptr(C, dp);
+    const uint32_t tc = d->tc;
+    d->tc = (lane == hit_idx ? (r | (tc & D_MULTI)) : tc) | D_PIN;
+  }
+  if (lane == 0)
+    for (uint32_t i = 32; i < npath; i++) {
+      DenseRec* d = d_ptr(C, C.w.rec()[C.w.path()[i]].dpos);
+      d->tc = (i == hit_idx ? (r | (d->tc & D_MULTI)) : d->tc) | D_PIN;
+    }
+  if (hit != NIL) C.c_wr += 1;
+  __syncwarp();
 
   // Step 3: speculative insertion of the input (R8, R9).
   const uint32_t m_in = min(m, L_in);
@@ -1040,12 +1089,6 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   const uint64_t d_bytes = C.m.kvt * (uint64_t)(n - m) + C.m.ssmb * n_ck;
   const uint32_t d_nodes = (p_split != NIL ? 1u : 0u) + (split_m ? 1u : 0u) + (split_n ? 1u : 0u) + (leaf ? 1u : 0u);
 
-  // Step 5: touch only the hit node.
-  if (hit != NIL) {
-    if (lane == 0) d_stamp(C, hit_dpos, r);
-    C.c_wr += 1;
-  }
-  __syncwarp();
   PHASE_MARK(C.t_walk);
 
   // Step 6: admission precheck (R12).
@@ -1076,7 +1119,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
           W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
           C.w.rec()[w] = W;
           C.w.ids()[w] = C.next_id++;
-          hash_insert_1(C, attach, ft, w);
+          hash_insert_1(C, hmake(C, attach, ft, w, n, true, (uint32_t)off), attach);
           NodeRec& Wa = C.w.rec()[attach];
           Wa.nf = Ra.nf + 1;
           Wa.cxor = Ra.cxor ^ w;
