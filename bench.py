@@ -4,10 +4,13 @@
 Metric (BASELINE.json): "requests replayed/sec × α-candidates at 1/2/4/8 B200;
 HBM GB/s vs peak".  Workload: BASELINE.json configs[2] -- the ShareGPT-shaped
 50k-request trace, 7B hybrid {4,24,28}, 60 GB cache, 16-value α grid x 128
-trace segments = 2,048 chains, sharded over N GPUs (strong scaling: the same
-chain list at every N).  A step = one replay of every chain of this rank's
-shard from its segment snapshot + the NCCL all-gather of per-α hit sums + α*
-selection.
+trace segments = 2,048 chains.  At N GPUs: N independent problems of that shape
+(trace seeds k = 0..N-1; weak scaling), the chains of every problem
+LPT-sharded across all ranks.  A step = replay of this rank's chains from their
+segment snapshots + one NCCL all-gather of per-(problem, α) hit sums + α*
+selection.  Why weak: a chain is sequential, and one
+problem's 2,048 chains already run concurrently on one B200, so a fixed chain
+list cannot get faster on more GPUs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3]
 
@@ -181,7 +184,7 @@ def reference_arm(args, w, config):
     v = tot_n / tot_t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64+f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
             "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{len(chains)} chains of the first {len(snaps)} segments per step"},
@@ -195,15 +198,20 @@ def reference_arm(args, w, config):
 def main():
     args = parse()
     import tracegen as tg
+    rank, world, local = dist_env()
+    n_prob = max(1, world) if args.impl == "b200" else 1
     t_gen = time.perf_counter()
-    w = tg.workload(args.config, R=args.requests or None)
+    ws = [tg.workload(args.config, R=args.requests or None, problem=k) for k in range(n_prob)]
     t_gen = time.perf_counter() - t_gen
+    w = ws[0]
     tr = w.trace
     config = {"workload": f"config{args.config} {w.name}-shaped trace, {tr.n_requests} requests, "
                           f"{len(w.variants)} cache variant(s), {len(w.alphas)} alphas x {len(w.segments())} "
-                          f"segments = {w.n_chains} chains",
+                          f"segments = {w.n_chains} chains" +
+                          (f"; x {n_prob} independent problems (one per GPU, weak scaling)" if n_prob > 1 else ""),
               "requests": tr.n_requests, "tokens": tr.n_tokens, "alphas": len(w.alphas),
-              "segments": len(w.segments()), "chains": w.n_chains, "window": w.window,
+              "segments": len(w.segments()), "chains": w.n_chains * n_prob, "window": w.window,
+              "problems": n_prob,
               "model": "7B hybrid {4 attn, 24 ssm, 28 mlp}, D=4096, N=128, fp16" if args.config in (2, 3, 4)
               else "see tracegen.workload", "cache_bytes": [v.capacity_bytes for v in w.variants],
               "l2": "flushed (256 MiB write) between timed steps, outside the event window"}
@@ -212,7 +220,6 @@ def main():
 
     import torch
     import torch.distributed as dist
-    rank, world, local = dist_env()
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
@@ -220,27 +227,51 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2411_19379_b200 import AlphaGrid
-    from paper_2411_19379_b200 import marconi as M
+    from paper_2411_19379_b200.grid import gather_hit_sums
 
+    # N problems (weak scaling): the chains of EVERY problem are LPT-sharded across all
+    # ranks, so each rank replays ~one problem's worth of chains and the per-(problem, α)
+    # hit sums must be all-gathered before any rank can pick α*.
     t_setup = time.perf_counter()
-    g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments, rank=rank, world=world, device=local)
-    g.setup()
+    gs = []
+    for k, wk in enumerate(ws):
+        g = AlphaGrid(wk.trace, wk.variants, wk.alphas, wk.n_segments, rank=rank, world=world, device=local)
+        g.setup()
+        gs.append(g)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream()
-    out = g.ctx.alloc_outputs(len(w.alphas), counters=True)
+    streams = [torch.cuda.Stream() for _ in gs] if len(gs) > 1 else [stream]
+    outs = [g.ctx.alloc_outputs(len(w.alphas), counters=True) for g in gs]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    my_reqs = int(sum(g.segs[c % len(g.segs)][1] for c in g.chains))
-    all_reqs = sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants)
+    my_reqs = sum(int(sum(g.segs[c % len(g.segs)][1] for c in g.chains)) for g in gs)
+    all_reqs = sum(sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants) for g in gs)
 
-    def step():
-        out["hit_sum"].zero_()
-        g.run(out=out)
-        return g.select(out)
+    def launch():
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        ends = []
+        for g, o, s in zip(gs, outs, streams):
+            s.wait_event(ev)
+            with torch.cuda.stream(s):
+                o["hit_sum"].zero_()
+                g.run(out=o, stream=s)
+                e = torch.cuda.Event()
+                e.record(s)
+                ends.append(e)
+        for e in ends:
+            stream.wait_event(e)
+
+    def select():
+        hs = torch.stack([o["hit_sum"] for o in outs])          # [problem, variant, alpha]
+        tot = gather_hit_sums(hs, world)                        # one all-gather over NCCL
+        return [g.select(o, gathered=tot[k]) for k, (g, o) in enumerate(zip(gs, outs))]
 
     for _ in range(args.warmup):
-        step()
-    g.ctx.check()
+        launch()
+        select()
+    for g in gs:
+        g.ctx.check()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -255,10 +286,9 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        out["hit_sum"].zero_()
-        g.run(out=out)               # replay_kernel on `stream`
+        launch()                     # replay_kernel per problem, concurrently on their streams
         e1.record(stream)
-        a_star = g.select(out)       # D2H + all-gather + argmax
+        a_star = select()            # all-gather + D2H + argmax
         e2.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e2))
@@ -267,7 +297,8 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    g.ctx.check()
+    for g in gs:
+        g.ctx.check()
     tot = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -275,8 +306,10 @@ def main():
     value = all_reqs * args.steps / (T_ms / 1000.0)
 
     # roofline of the dominant kernel (replay_kernel) from the device counters of this rank
-    ctr = out["counters"].cpu().numpy()[g.chains.astype(np.int64)]
-    alg_bytes = algorithmic_bytes(ctr, my_reqs)
+    alg_bytes = 0
+    for g, o in zip(gs, outs):
+        ctr = o["counters"].cpu().numpy()[g.chains.astype(np.int64)]
+        alg_bytes += algorithmic_bytes(ctr, int(sum(g.segs[c % len(g.segs)][1] for c in g.chains)))
     kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1000.0
     peak, peak_kind = peaks()
     achieved = alg_bytes / kern_avg_s / 1e9
@@ -290,10 +323,10 @@ def main():
         except Exception:
             traffic = None
 
-    # e2e through the public API with host buffers (rank-local shard)
+    # e2e through the public API with host buffers (this rank's shards of every problem)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_measure(g, w, args, out)
+        e2e = e2e_measure(gs, ws, args, outs)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -303,9 +336,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": dict(config, parallelism=f"chains sharded over {world} GPU(s) (LPT), NCCL all-gather of "
-                                                 f"per-alpha hit sums", alpha_star=a_star,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+            "config": dict(config, parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one NCCL "
+                                                 f"all-gather of per-(problem, alpha) hit sums per step",
+                           alpha_star=[a[0] for a in a_star],
                            setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -313,7 +347,7 @@ def main():
                          "launch_ms": kern_avg_s * 1000.0},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,  # one replay_kernel launch per step
+            "gpu_launches": args.steps * len(gs),  # one replay_kernel launch per problem per step
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -321,34 +355,37 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_measure(g, w, args, out):
-    """Same metric end to end through the C ABI from pinned host buffers: per step H2D of the trace
-    (tokens + requests) and the segment snapshots, the replay, D2H of per-request hits and hit sums."""
+def e2e_measure(gs, ws, args, outs):
+    """Same metric end to end through the C ABI from host buffers: per step, for every
+    problem, H2D of the trace (tokens + requests, pinned) and of the segment snapshots,
+    the replay of this rank's chains, D2H of the per-request hits and the hit sums."""
     import torch
     from paper_2411_19379_b200 import marconi as M
-    tr = w.trace
-    ctx = g.ctx
-    h_tok = torch.from_numpy(np.ascontiguousarray(tr.tokens, np.uint32).view(np.int32)).pin_memory()
-    h_req = torch.from_numpy(M.requests_array(tr.off, tr.lin, tr.lout).view(np.int64)).pin_memory()
-    snaps = [ctx.get_snapshot(0, k) for k in range(ctx.snapshot_count(0))]
-    d_tok = torch.empty_like(h_tok, device="cuda")
-    d_req = torch.empty_like(h_req, device="cuda")
-    h_hit = torch.empty(out["hit"].shape, dtype=torch.int32).pin_memory()
-    snap_bytes = sum(len(s[0]) for s in snaps) * M.SNAP_DTYPE.itemsize
-    h2d = h_tok.numel() * 4 + h_req.numel() * 8 + snap_bytes
-    d2h = h_hit.numel() * 4 + out["hit_sum"].numel() * 8
-    stream = torch.cuda.current_stream()
-    n_units = sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants)
+    st = []
+    for g, wk, o in zip(gs, ws, outs):
+        tr = wk.trace
+        ctx = g.ctx
+        h_tok = torch.from_numpy(np.ascontiguousarray(tr.tokens, np.uint32).view(np.int32)).pin_memory()
+        h_req = torch.from_numpy(M.requests_array(tr.off, tr.lin, tr.lout).view(np.int64)).pin_memory()
+        snaps = [ctx.get_snapshot(0, k) for k in range(ctx.snapshot_count(0))]
+        d_tok = torch.empty_like(h_tok, device="cuda")
+        d_req = torch.empty_like(h_req, device="cuda")
+        h_hit = torch.empty(o["hit"].shape, dtype=torch.int32).pin_memory()
+        st.append((g, tr, ctx, o, h_tok, h_req, snaps, d_tok, d_req, h_hit))
+    h2d = sum(x[4].numel() * 4 + x[5].numel() * 8 + sum(len(s[0]) for s in x[6]) * M.SNAP_DTYPE.itemsize for x in st)
+    d2h = sum(x[9].numel() * 4 + x[3]["hit_sum"].numel() * 8 for x in st)
+    n_units = sum(sum(n for _, n, _ in g.segs) * len(wk.alphas) * len(wk.variants) for g, wk in zip(gs, ws))
 
     def one():
-        d_tok.copy_(h_tok, non_blocking=True)
-        d_req.copy_(h_req, non_blocking=True)
-        ctx.set_trace_device(d_tok, d_req, tr.n_requests)
-        ctx.set_snapshots(0, snaps)
-        out["hit_sum"].zero_()
-        g.run(out=out)
-        h_hit.copy_(out["hit"], non_blocking=True)
-        g.select(out)
+        for g, tr, ctx, o, h_tok, h_req, snaps, d_tok, d_req, h_hit in st:
+            d_tok.copy_(h_tok, non_blocking=True)
+            d_req.copy_(h_req, non_blocking=True)
+            ctx.set_trace_device(d_tok, d_req, tr.n_requests)
+            ctx.set_snapshots(0, snaps)
+            o["hit_sum"].zero_()
+            g.run(out=o)
+            h_hit.copy_(o["hit"], non_blocking=True)
+            g.select(o)
         torch.cuda.synchronize()
 
     for _ in range(2):
@@ -365,7 +402,7 @@ def e2e_measure(g, w, args, out):
         dt = float(t[0])
     return {"value": n_units * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "note": "wall clock incl. H2D of trace+requests+snapshots (pinned/pageable host) and D2H of hits"}
+            "note": "wall clock incl. H2D of trace+requests (pinned) and snapshots, D2H of per-request hits"}
 
 
 if __name__ == "__main__":

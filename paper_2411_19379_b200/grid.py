@@ -129,7 +129,11 @@ class AlphaGrid:
         costs = chain_costs(lens, self.segs, len(self.variants), len(self.alphas))
         self.shards = lpt_shard(costs, len(self.segs), len(self.alphas), self.world)
         self.chains = self.shards[self.rank]
-        self.workspace = self.ctx.alloc_workspace(0, len(self.alphas), len(self.chains))
+        dflt = self.ctx.workspace_size(0, len(self.alphas), len(self.chains))
+        one = self.ctx.workspace_size(1, len(self.alphas), len(self.chains))
+        per = self.ctx.workspace_size(2, len(self.alphas), len(self.chains)) - one
+        workers = min(max(1, len(self.chains)), (dflt - one) // per + 1)
+        self.workspace = self.ctx.alloc_workspace(workers, len(self.alphas), len(self.chains))
         return self
 
     @property
@@ -139,7 +143,7 @@ class AlphaGrid:
     def run(self, out=None, **kw):
         return self.ctx.replay(self.alphas, chains=self.chains, workspace=self.workspace, out=out, **kw)
 
-    def select(self, out) -> List[float]:
-        hs = gather_hit_sums(out["hit_sum"], self.world, self.group)
+    def select(self, out, gathered=None) -> List[float]:
+        hs = gathered if gathered is not None else gather_hit_sums(out["hit_sum"], self.world, self.group)
         self.hit_sums = hs.cpu().numpy()
         return select_alpha(self.alphas, self.hit_sums)

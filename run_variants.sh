@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -2 gpurun_out/pytest_gpu.log
-for f in build/variants/*.so; do
-  PHASES=1 MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -2
-done | tee gpurun_out/variants.txt
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.jsonl 2> gpurun_out/bench.err; echo "bench rc=$?"
+tail -1 gpurun_out/bench.jsonl | cut -c1-600; tail -3 gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.jsonl 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref.jsonl | cut -c1-400

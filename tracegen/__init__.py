@@ -473,9 +473,11 @@ GB = 1_000_000_000
 UNLIMITED_BYTES = (1 << 64) - 1   # "bytes unlimited" (toy config: node-count capacity only)
 
 
-def workload(cfg: int, R: Optional[int] = None) -> Workload:
-    """Build config `cfg` (1..5).  R overrides the request count (for small parity runs)."""
-    seed = 1000 + cfg
+def workload(cfg: int, R: Optional[int] = None, problem: int = 0) -> Workload:
+    """Build config `cfg` (1..5).  R overrides the request count (for small parity runs).
+    problem > 0 draws an independent trace of the same shape (seed offset), used by the
+    weak-scaling bench (one α-tuning problem per GPU)."""
+    seed = 1000 + cfg + 7919 * problem
     if cfg == 1:
         tr = toy_trace(seed, R or 16)
         return Workload("toy", tr, [Variant(MODEL_TOY, UNLIMITED_BYTES, 6)], (0.0, 1.0), 1)
