@@ -135,6 +135,14 @@ mc_status mc_set_snapshots(mc_ctx* ctx, uint32_t variant, const mc_snap_node* h_
 mc_status mc_live_pass(mc_ctx* ctx, uint32_t window, void* d_workspace, uint64_t workspace_bytes,
                        uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, void* stream);
 
+/* General form: snapshot k = the tree after request h_points[k] (h_points[0] = 0,
+ * strictly increasing, <= n_reqs).  h_first_evict (host, nullable) receives per
+ * variant the first request whose admission evicted a node (0 = none) -- the point
+ * where the paper takes its tuning snapshot (§4.2 "Managing the balance"). */
+mc_status mc_live_pass_at(mc_ctx* ctx, const uint32_t* h_points, uint32_t n_points, void* d_workspace,
+                          uint64_t workspace_bytes, uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass,
+                          uint32_t* h_first_evict, void* stream);
+
 /* Number of snapshots held for a variant and copy one back as canonical
  * records sorted by id (host).  *n_out receives the record count; h_out may be
  * NULL to query it. */

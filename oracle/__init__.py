@@ -279,3 +279,45 @@ def select_alpha(alphas: Sequence[float], hit_sums: Sequence[int]) -> float:
         if best is None or s > best[1]:
             best = (a, s)
     return best[0]
+
+
+def live_tune(trace, variant, alphas: Sequence[float], multiplier: int = 10, n_threads: int = 0):
+    """The paper's tuning loop on the oracle, step by step:
+    α = 0 until the first request r_F whose admission evicted; snapshot; α = 0 over the
+    bootstrap window (r_F, r_F + multiplier*r_F]; grid replay of that window from the
+    snapshot; adopt α* for the rest.  Returns (hits, flops, info)."""
+    R = trace.n_requests
+    o = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, 0.0)
+    hits = np.zeros(R, np.uint32)
+    flops = np.zeros(R, np.uint64)
+    r_f = 0
+    snap = None
+    for r in range(1, R + 1):
+        h, f, _ = o.step(r)
+        hits[r - 1], flops[r - 1] = h, f
+        if r_f == 0 and len(o.log()) > 0:
+            r_f = r
+            snap = o.dump()
+            break
+    info = {"r_first_evict": r_f, "alpha_star": 0.0, "window": None, "grid_hit_sums": None}
+    if r_f == 0 or r_f >= R:  # never evicted (the loop ran to R) or evicted only at the end
+        o.close()
+        return hits, flops, info
+    b_end = min(r_f + multiplier * r_f, R)
+    info["window"] = (r_f + 1, b_end)
+    h, f, _ = o.run(r_f + 1, b_end - r_f)           # live α = 0 bootstrap
+    hits[r_f:b_end], flops[r_f:b_end] = h, f
+    end_snap = o.dump() if b_end < R else None
+    o.close()
+    chains = [(0, a, r_f + 1, b_end - r_f, 0) for a in alphas]
+    _, _, _, hs, _ = run_chains(trace, [variant], chains, [snap], n_threads=n_threads)
+    a_star = select_alpha(alphas, [int(x) for x in hs])
+    info["alpha_star"] = a_star
+    info["grid_hit_sums"] = [int(x) for x in hs]
+    if b_end < R:
+        o2 = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, a_star)
+        o2.load(*end_snap)
+        h, f, _ = o2.run(b_end + 1, R - b_end)
+        hits[b_end:], flops[b_end:] = h, f
+        o2.close()
+    return hits, flops, info

@@ -6,4 +6,4 @@ PyTorch supplies device memory, streams and the NCCL process group only.
 """
 from . import marconi  # noqa: F401
 from .marconi import Context, MarconiError  # noqa: F401
-from .grid import AlphaGrid, lpt_shard, select_alpha  # noqa: F401
+from .grid import AlphaGrid, LiveTuner, lpt_shard, select_alpha  # noqa: F401

@@ -113,18 +113,25 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
+  uint32_t next = 1, first = 0;
   Prefetched cur = fetch_request(P, 1), nxt = cur;
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
+    const uint32_t ev0 = C.n_evict;
     const ReqOut o = process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
     cur = nxt;
+    if (first == 0 && C.n_evict != ev0) first = r;  // the paper's "first eviction"
     if (lane == 0) {
       const uint64_t k = (uint64_t)v * P.n_req + r - 1;
       if (P.hit) P.hit[k] = o.reuse;
       if (P.flops) P.flops[k] = o.flops;
       if (P.bypass) P.bypass[k] = o.bypass ? 1 : 0;
     }
-    if (r % P.window == 0 && r < P.n_req) dump_snapshot(C, P, out, r / P.window);
+    while (next < P.n_points && P.live_points[next] == r) {
+      dump_snapshot(C, P, out, next);
+      next++;
+    }
   }
+  if (lane == 0 && P.first_evict) P.first_evict[v] = first;
 }
 
 // parent_idx of uploaded canonical records (sorted by id within each snapshot).
@@ -227,6 +234,7 @@ struct mc_ctx {
   mc_segment* d_segs = nullptr;
   uint32_t* d_status = nullptr;
   double* d_alphas = nullptr;  // small device buffer (64 entries)
+  uint32_t* d_points = nullptr;  // live-pass snapshot points + first-eviction outputs
   uint32_t alpha_cap = 0;
 };
 
@@ -352,6 +360,7 @@ void mc_destroy(mc_ctx* c) {
   cudaFree(c->d_segs);
   cudaFree(c->d_status);
   cudaFree(c->d_alphas);
+  cudaFree(c->d_points);
   delete c;
 }
 
@@ -462,14 +471,19 @@ mc_status mc_workspace_workers(const mc_ctx* c, uint64_t bytes, uint32_t n_alpha
   return MC_OK;
 }
 
-mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,
-                       uint64_t* d_flops, uint8_t* d_bypass, void* stream) {
-  if (!c || !d_ws || window == 0) return fail(MC_EINVAL, "mc_live_pass: bad argument");
+mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points, void* d_ws, uint64_t ws_bytes,
+                          uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict,
+                          void* stream) {
+  if (!c || !d_ws || !h_points || n_points == 0) return fail(MC_EINVAL, "mc_live_pass_at: bad argument");
   if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
+  if (h_points[0] != 0) return fail(MC_EINVAL, "snapshot point 0 must be 0 (the empty tree)");
+  for (uint32_t k = 1; k < n_points; k++)
+    if (h_points[k] <= h_points[k - 1] || h_points[k] > c->n_req)
+      return fail(MC_EINVAL, "snapshot points must be strictly increasing request indices <= n_reqs");
   const uint32_t nv = (uint32_t)c->hv.size();
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
   if (ws_bytes < kCtrl + per * nv) return fail(MC_ENOMEM, "workspace too small for the live pass");
-  const uint32_t K = (c->n_req + window - 1) / window;
+  const uint32_t K = n_points;
   std::vector<DevSnapOut> outs(nv);
   for (uint32_t v = 0; v < nv; v++) {
     SnapStore& s = c->snaps[v];
@@ -494,10 +508,14 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
     outs[v].count = K;
     outs[v].pad = 0;
   }
+  cudaFree(c->d_points);
+  c->d_points = nullptr;
+  CU(cudaMalloc(&c->d_points, sizeof(uint32_t) * (K + nv)));
   cudaStream_t st = (cudaStream_t)stream;
   DevSnapOut* d_outs = (DevSnapOut*)((char*)d_ws + 256);
   if (sizeof(DevSnapOut) * nv + 256 > kCtrl) return fail(MC_EINVAL, "too many variants for the live pass");
   CU(cudaMemcpyAsync(d_outs, outs.data(), sizeof(DevSnapOut) * nv, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(c->d_points, h_points, sizeof(uint32_t) * K, cudaMemcpyHostToDevice, st));
   KParams P;
   memset(&P, 0, sizeof(P));
   P.tok = c->tok;
@@ -516,7 +534,9 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
   P.bypass = d_bypass;
   P.status = c->d_status;
   P.live_out = d_outs;
-  P.window = window;
+  P.live_points = c->d_points;
+  P.n_points = K;
+  P.first_evict = c->d_points + K;
   P.smem_nodes = c->smem_nodes_live;
   live_kernel<<<nv, 32, 8ull * c->smem_nodes_live, st>>>(P);
   CU(cudaGetLastError());
@@ -524,8 +544,20 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
   std::vector<uint64_t> offK(1, (uint64_t)K * c->ncap);
   for (uint32_t v = 0; v < nv; v++)
     CU(cudaMemcpyAsync(c->snaps[v].off + K, offK.data(), sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  if (h_first_evict)
+    CU(cudaMemcpyAsync(h_first_evict, c->d_points + K, sizeof(uint32_t) * nv, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return upload_stores(c);
+}
+
+mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,
+                       uint64_t* d_flops, uint8_t* d_bypass, void* stream) {
+  if (!c || window == 0) return fail(MC_EINVAL, "mc_live_pass: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
+  std::vector<uint32_t> pts;
+  for (uint64_t r = 0; r < c->n_req; r += window) pts.push_back((uint32_t)r);
+  return mc_live_pass_at(c, pts.data(), (uint32_t)pts.size(), d_ws, ws_bytes, d_hit, d_flops, d_bypass, nullptr,
+                         stream);
 }
 
 mc_status mc_snapshot_count(const mc_ctx* c, uint32_t variant, uint32_t* n_out) {

@@ -129,7 +129,9 @@ struct KParams {
   uint32_t* status;
   // live pass
   DevSnapOut* live_out;
-  uint32_t window;
+  const uint32_t* live_points;  // snapshot k = tree after request live_points[k] (ascending, [0] = 0)
+  uint32_t n_points;
+  uint32_t* first_evict;        // [n_var] first request whose admission evicted (0 = none)
   uint32_t smem_nodes;  // dense positions held in shared memory per warp
 };
 
@@ -256,6 +258,7 @@ struct Chain {
   uint32_t capn;
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
+  uint32_t n_evict;   // evictions so far (uniform)
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   unsigned long long t_walk, t_evict, t_insert, t_unpin;
 #endif
@@ -832,6 +835,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
   Bounds b;
   const Best best = select_victim(C, cnt, b);
   C.c_scan += cnt;
+  C.n_evict++;
   if (best.i == NIL) {
     if (lane == 0) atomicOr(P.status, ST_NOCAND);
     C.failed = true;
@@ -1181,6 +1185,7 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.capn = V.cap_nodes;
   C.alpha = alpha;
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
+  C.n_evict = 0;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   C.t_walk = C.t_evict = C.t_insert = C.t_unpin = 0;
 #endif

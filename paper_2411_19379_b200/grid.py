@@ -147,3 +147,64 @@ class AlphaGrid:
         hs = gathered if gathered is not None else gather_hit_sums(out["hit_sum"], self.world, self.group)
         self.hit_sums = hs.cpu().numpy()
         return select_alpha(self.alphas, self.hit_sums)
+
+
+class LiveTuner:
+    """The paper's online α tuning loop on the device (§4.2 "Managing the balance",
+    PAPER:426-427), one cache variant:
+
+    1. α = 0 (LRU) from an empty cache until the first request r_F whose
+       admission evicted a node; snapshot the tree after r_F;
+    2. bootstrap: keep α = 0 for the next multiplier * r_F requests (10x, reading R16);
+    3. grid: replay the bootstrap window from the snapshot for every α; α* = argmax of
+       hit tokens (ties -> smallest α);
+    4. adopt α* for the rest of the trace (replayed from the tree at the end of the
+       bootstrap).
+    If no eviction ever happens, or the window is empty, α stays 0.
+    Every step runs in the CUDA kernels (live pass, replays); this class only sequences them.
+    """
+
+    def __init__(self, trace, variant, alphas, multiplier: int = 10, max_nodes: int = 8192, device: int = 0):
+        self.trace = trace
+        self.variant = variant
+        self.alphas = [float(a) for a in alphas]
+        self.multiplier = multiplier
+        self.ctx = M.Context([variant], max_nodes=max_nodes, device=device)
+
+    def run(self):
+        import torch
+        tr = self.trace
+        R = tr.n_requests
+        self.ctx.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
+        hit0, fl0, by0, fe = self.ctx.live_pass_at([0])
+        r_f = fe[0]
+        hits = hit0[0].cpu().numpy().copy()
+        flops = fl0[0].cpu().numpy().copy()
+        info = {"r_first_evict": r_f, "alpha_star": 0.0, "window": None, "grid_hit_sums": None}
+        if r_f == 0 or r_f >= R:
+            return hits, flops, info
+        b_end = min(r_f + self.multiplier * r_f, R)
+        info["window"] = (r_f + 1, b_end)
+        points = [0, r_f] + ([b_end] if b_end < R else [])
+        h1, f1, _, _ = self.ctx.live_pass_at(points)
+        segs = [(r_f + 1, b_end - r_f, 1)]
+        if b_end < R:
+            segs.append((b_end + 1, R - b_end, 2))
+        self.ctx.set_segments(segs)
+        ns, na = len(segs), len(self.alphas)
+        out = self.ctx.replay(self.alphas, chains=[a * ns for a in range(na)], log_cap=0)
+        self.ctx.check()
+        sums = out["hit_sum"].cpu().numpy()[0]
+        a_star = select_alpha(self.alphas, sums[None, :])[0]
+        info["alpha_star"] = a_star
+        info["grid_hit_sums"] = [int(x) for x in sums]
+        live_hits = h1[0].cpu().numpy()
+        hits[:b_end] = live_hits[:b_end]
+        flops[:b_end] = f1[0].cpu().numpy()[:b_end]
+        if b_end < R:
+            ai = self.alphas.index(a_star)
+            out2 = self.ctx.replay(self.alphas, chains=[ai * ns + 1], log_cap=0)
+            self.ctx.check()
+            hits[b_end:] = out2["hit"].cpu().numpy()[0, ai, b_end:]
+            flops[b_end:] = out2["flops"].cpu().numpy()[0, ai, b_end:]
+        return hits, flops, info

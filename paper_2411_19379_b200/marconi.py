@@ -25,7 +25,8 @@ EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n
                         ("utility", "<f8")], align=True)
 assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
 
-EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_snapshots", "mc_live_pass", "mc_snapshot_count",
+EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at",
+            "mc_snapshot_count",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
             "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin")
 
@@ -75,6 +76,7 @@ def lib():
             "mc_set_trace": [P, P, U64, P, U32],
             "mc_set_snapshots": [P, U32, P, P, P, U32, P],
             "mc_live_pass": [P, U32, P, U64, P, P, P, P],
+            "mc_live_pass_at": [P, P, U32, P, U64, P, P, P, P, P],
             "mc_snapshot_count": [P, U32, P],
             "mc_get_snapshot": [P, U32, U32, P, U64, P, P],
             "mc_set_segments": [P, P, U32],
@@ -232,6 +234,22 @@ class Context:
                                  _stream_ptr(stream)))
         self.check(stream)
         return hit, fl, by
+
+    def live_pass_at(self, points, workspace=None, stream=None):
+        """α = 0 live pass with snapshot k = tree after request points[k] (points[0] = 0).
+        Returns (hit, flops, bypass device tensors [n_var, R], first_evict list per variant)."""
+        torch = self.torch
+        nv = len(self.variants)
+        ws = workspace if workspace is not None else self.alloc_workspace(n_workers=nv)
+        hit = torch.zeros((nv, self.n_req), dtype=torch.int32, device=self.device)
+        fl = torch.zeros((nv, self.n_req), dtype=torch.int64, device=self.device)
+        by = torch.zeros((nv, self.n_req), dtype=torch.uint8, device=self.device)
+        pts = np.ascontiguousarray(points, np.uint32)
+        fe = np.zeros(nv, np.uint32)
+        check(lib().mc_live_pass_at(self.h, _np_ptr(pts), len(pts), _tptr(ws), ws.numel(), _tptr(hit), _tptr(fl),
+                                    _tptr(by), _np_ptr(fe), _stream_ptr(stream)))
+        self.check(stream)
+        return hit, fl, by, [int(x) for x in fe]
 
     # ---- segments ----
     def set_segments(self, segs):
