@@ -259,6 +259,7 @@ struct Chain {
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
+  uint32_t moved_slot, moved_pos;  // last eviction: node whose dense entry moved, and where
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   unsigned long long t_walk, t_evict, t_insert, t_unpin;
 #endif
@@ -274,6 +275,8 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.nfree = __shfl_sync(FULL, C.nfree, 0);
   C.c_wr = __shfl_sync(FULL, (unsigned long long)C.c_wr, 0);
   C.failed = __shfl_sync(FULL, (int)C.failed, 0);
+  C.moved_slot = __shfl_sync(FULL, C.moved_slot, 0);
+  C.moved_pos = __shfl_sync(FULL, C.moved_pos, 0);
 }
 
 __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_t mask) {
@@ -368,7 +371,10 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
 __device__ __forceinline__ DenseRec* d_ptr(const Chain& C, uint32_t i) { return i < C.S ? C.sd + i : C.w.tail() + i; }
 __device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return d_ptr(C, i)->tc; }
 __device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return C.w.eff64()[i]; }
-__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[C.w.dslot()[i]]; }
+// dense position -> slot (global: shared memory is reserved for the scanned dense words)
+__device__ __forceinline__ uint32_t d_slot(const Chain& C, uint32_t i) { return C.w.dslot()[i]; }
+__device__ __forceinline__ void d_set_slot(Chain& C, uint32_t i, uint32_t s) { C.w.dslot()[i] = s; }
+__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[d_slot(C, i)]; }
 __device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
 __device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
   C.w.eff64()[i] = v;
@@ -387,7 +393,7 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   const uint32_t i = C.count++;
   NodeRec& R = C.w.rec()[s];
   R.dpos = i;
-  C.w.dslot()[i] = s;
+  d_set_slot(C, i, s);
   d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
   d_set_tc(C, i, t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u));
 }
@@ -462,7 +468,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     R.dpos = i;
     C.w.rec()[s] = R;
     C.w.ids()[s] = r.id;
-    C.w.dslot()[i] = s;
+    d_set_slot(C, i, s);
     bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
@@ -516,7 +522,7 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
   mc_snap_node* dst = out->nodes + (uint64_t)k * out->stride;
   uint32_t* pdst = out->pidx + (uint64_t)k * out->stride;
   for (uint32_t i = lane; i < C.count; i += 32) {
-    const uint32_t s = C.w.dslot()[i];
+    const uint32_t s = d_slot(C, i);
     const NodeRec R = C.w.rec()[s];
     const uint32_t p = R.parent;
     mc_snap_node r;
@@ -664,7 +670,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
         }
       }
     });
-    if (best.i != NIL) best.slot = C.w.dslot()[best.i];  // prefetch for the removal
+    if (best.i != NIL) best.slot = d_slot(C, best.i);  // for the removal
     // resolve ids only when lanes tie on the minimum t
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -771,7 +777,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   const double pre_lo = (nlo == 1) ? e64[ilo] : 0.0;
   const double pre_hi = (nhi == 1) ? e64[ihi] : 0.0;
   const double pre_k1 = (i1 != NIL) ? e64[i1] : 0.0;
-  const uint32_t pre_slot = (i1 != NIL) ? C.w.dslot()[i1] : NIL;
+  const uint32_t pre_slot = (i1 != NIL) ? d_slot(C, i1) : NIL;
   double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
   if (__any_sync(FULL, nlo > 1 || nhi > 1)) {
     // several entries share an fp32 extreme: read all of their fp64 values (cold path)
@@ -801,6 +807,9 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   if (!exact_only && !__any_sync(FULL, (double)k2 <= lim)) {
     const bool mine = (double)k1 <= lim;
     if (mine) {
+#ifdef MC_PREFETCH_VICTIM
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(C.w.rec() + pre_slot));  // the removal reads it next
+#endif
       best.t = d_tc(C, i1);
       best.u = utility(b, best.t, pre_k1, C.alpha);
       best.i = i1;
@@ -845,9 +854,9 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     // Loads first (independent ones back to back), then the stores: every store
     // below targets fields no later load in this block reads.
     const uint32_t last = cnt - 1;
-    const uint32_t sl = C.w.dslot()[last];      // node moved into the freed dense position
+    const uint32_t sl = d_slot(C, last);        // node moved into the freed dense position
     const double e_last = C.w.eff64()[last];
-    const uint32_t x = (best.slot != NIL) ? best.slot : C.w.dslot()[best.i];
+    const uint32_t x = (best.slot != NIL) ? best.slot : d_slot(C, best.i);
     const NodeRec X = C.w.rec()[x];
     const uint32_t p = X.parent;
     const uint32_t xf = X.nf >> 24;
@@ -895,10 +904,13 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     }
     // dense_remove: move the last dense entry into the victim's position
     const uint32_t i = X.dpos;
+    C.moved_slot = NIL;
     if (i != last) {
+      C.moved_slot = sl;
+      C.moved_pos = i;
       *d_ptr(C, i) = *d_ptr(C, last);
       C.w.eff64()[i] = e_moved;
-      C.w.dslot()[i] = sl;
+      d_set_slot(C, i, sl);
       C.w.rec()[sl].dpos = i;
     }
     C.count = last;
@@ -1049,9 +1061,10 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
 
   // Pin the path (R12) and touch only the hit node (step 5): every path
   // lane reads its node's dense position and updates its dense word in parallel.
+  uint32_t my_dp = NIL;
   if (lane < min(npath, 32u)) {
-    const uint32_t dp = C.w.rec()[my_path].dpos;
-    DenseRec* d = d_ptr(C, dp);
+    my_dp = C.w.rec()[my_path].dpos;
+    DenseRec* d = d_ptr(C, my_dp);
     const uint32_t tc = d->tc;
     d->tc = (lane == hit_idx ? (r | (tc & D_MULTI)) : tc) | D_PIN;
   }
@@ -1099,8 +1112,10 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   const bool bypass = (pinned_bytes + d_bytes > C.capb) || (C.capn && npath + d_nodes > C.capn);
   if (!bypass) {
     // Step 7: evict the argmin utility until the request fits.
-    while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + d_nodes > C.capn)))
+    while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + d_nodes > C.capn))) {
       evict_one(C, P, r, log, log_n);
+      if (my_path == C.moved_slot && C.moved_slot != NIL) my_dp = C.moved_pos;  // keep the pin target current
+    }
     PHASE_MARK(C.t_evict);
     // Step 8: insert.
     if (lane == 0 && !C.failed) {
@@ -1147,8 +1162,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   PHASE_MARK(C.t_insert);
   // Step 9: unpin (every path lane clears its node's pin bit in parallel), outputs.
   if (lane < min(npath, 32u)) {
-    const uint32_t dp = C.w.rec()[my_path].dpos;
-    DenseRec* d = d_ptr(C, dp);
+    DenseRec* d = d_ptr(C, my_dp);
     d->tc &= ~D_PIN;
   }
   if (lane == 0) {
@@ -1186,6 +1200,8 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.alpha = alpha;
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;
+  C.moved_slot = NIL;
+  C.moved_pos = 0;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   C.t_walk = C.t_evict = C.t_insert = C.t_unpin = 0;
 #endif
