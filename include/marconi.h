@@ -67,12 +67,16 @@ typedef struct {
 
 /* One cache configuration.  capacity_bytes = UINT64_MAX means unlimited bytes,
  * 0 = no cache (every request bypasses admission).  capacity_nodes
- * caps the number of non-root nodes (0 = no node cap; the toy config uses 6). */
+ * caps the number of non-root nodes (0 = no node cap; the toy config uses 6).
+ * chunk_size = 0: exact checkpoint positions (two-pass prefill);
+ * chunk_size = c > 0: chunked state passing -- the prefill (branch) checkpoint is
+ * placed at the multiple of c at or below the branch point and skipped if that is 0
+ * or not beyond the hit; decode checkpoints stay exact. */
 typedef struct {
   mc_model model;
   uint64_t capacity_bytes;
   uint32_t capacity_nodes;
-  uint32_t reserved;
+  uint32_t chunk_size;
 } mc_variant;
 
 /* Request r (1-based, at index r-1): sequence = tokens[tok_off, tok_off + input_len

@@ -153,6 +153,7 @@ struct Oracle {
   orc_model model;
   u64 cap_bytes;
   u32 cap_nodes;  // 0 = no node cap
+  u32 chunk = 0;  // 0 = exact checkpoint positions; else chunk-aligned prefill checkpoints (NEXT-3)
   double alpha;
   const u32* tokens;
   u64 n_tokens;
@@ -240,17 +241,35 @@ struct Oracle {
 
     // Step 3: speculative insertion of the input (fig:spec_insertion) [c.3 #8, #9].
     const u64 m_in = std::min(m, L_in);
-    u64 p = 0;                 // branch position, 0 = none
-    Node* p_split = nullptr;   // node whose edge strictly contains p
-    Node* p_gain = nullptr;    // existing node ending at p that lacks SSM
+    u64 q = 0;                 // branch position found by the dry-run insertion, 0 = none
     if (m_in > 0) {
       for (Node* x : path) {
         u64 de = depth_of(x), ds = de - x->edge.size();
         if (x != partial && de == m_in) {
-          if (!x->has_ssm) { p = m_in; p_gain = x; }
+          if (!x->has_ssm) q = m_in;
           break;
         }
-        if (ds < m_in && m_in < de) { p = m_in; p_split = x; break; }
+        if (ds < m_in && m_in < de) { q = m_in; break; }
+      }
+    }
+    // Chunked state passing (NEXT-3): the prefill checkpoint moves down to
+    // the chunk boundary at or below q; skipped if that is 0 or not beyond the hit.
+    u64 p = q;
+    if (q && chunk) {
+      p = (q / chunk) * chunk;
+      if (p == 0 || p <= reuse) p = 0;
+    }
+    Node* p_split = nullptr;   // node whose edge strictly contains p
+    Node* p_gain = nullptr;    // existing node ending at p that lacks SSM
+    if (p) {
+      for (Node* x : path) {
+        u64 de = depth_of(x), ds = de - x->edge.size();
+        if (x != partial && de == p) {
+          if (!x->has_ssm) p_gain = x;
+          else p = 0;  // the state already exists
+          break;
+        }
+        if (ds < p && p < de) { p_split = x; break; }
       }
     }
 
@@ -581,6 +600,7 @@ void* orc_create(const orc_model* m, u64 cap_bytes, u32 cap_nodes, double alpha,
   }
 }
 void orc_destroy(void* h) { delete (Oracle*)h; }
+int orc_set_chunk(void* h, u32 chunk) { ORC_TRY(((Oracle*)h)->chunk = chunk) }
 int orc_set_alpha(void* h, double a) {
   ORC_TRY(if (!(a >= 0)) throw std::invalid_argument("alpha < 0"); ((Oracle*)h)->alpha = a)
 }
@@ -624,7 +644,7 @@ int orc_total(void* h, u64* total, u64* count) {
 // first[c] .. first[c]+n[c]-1 at alpha[c] from snapshot
 // snap_nodes[snap_off[s] .. snap_off[s+1]) with s = snap_idx[c]; outputs are
 // written at hit[out_off[c] + i].  hit_sum[c] = sum of hits.
-int orc_run_chains(const orc_model* models, const u64* cap_bytes, const u32* cap_nodes,
+int orc_run_chains(const orc_model* models, const u64* cap_bytes, const u32* cap_nodes, const u32* chunks,
                    const u32* variant, const double* alpha, const u32* first, const u32* n,
                    const u32* snap_idx, const orc_node* snap_nodes, const u64* snap_off,
                    const u32* snap_next_id, u32 n_chains, const u32* tokens, u64 n_tokens,
@@ -645,6 +665,7 @@ int orc_run_chains(const orc_model* models, const u64* cap_bytes, const u32* cap
           Oracle* o = (Oracle*)orc_create(&models[v], cap_bytes[v], cap_nodes[v], alpha[c], tokens,
                                           n_tokens, off, lin, lout, n_req);
           if (!o) throw std::runtime_error(g_err);
+          o->chunk = chunks ? chunks[v] : 0;
           u32 s = snap_idx[c];
           o->load(snap_nodes + snap_off[s], (u32)(snap_off[s + 1] - snap_off[s]), snap_next_id[s]);
           u64 sum = 0;

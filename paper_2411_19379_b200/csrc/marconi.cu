@@ -330,7 +330,7 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     d.m = make_model(hv[v].model);
     d.cap_bytes = hv[v].capacity_bytes;
     d.cap_nodes = hv[v].capacity_nodes;
-    d.pad = 0;
+    d.chunk = hv[v].chunk_size;
     c->dvh.push_back(d);
   }
   c->snaps.resize(n_var);

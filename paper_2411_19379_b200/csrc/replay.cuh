@@ -71,7 +71,7 @@ struct DevModel {
 struct DevVariant {
   DevModel m;
   uint64_t cap_bytes;
-  uint32_t cap_nodes, pad;
+  uint32_t cap_nodes, chunk;  // chunk = 0: exact checkpoints; else chunk-aligned prefill checkpoints
 };
 struct DevSnapStore {
   const mc_snap_node* nodes;
@@ -255,7 +255,7 @@ struct Chain {
   uint32_t next_id, hwm, nfree;
   DevModel m;
   uint64_t capb;
-  uint32_t capn;
+  uint32_t capn, chunk;
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
@@ -1000,7 +1000,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
-  uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL;
+  uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL, my_ds = 0, my_de = 0, my_fl = 0;
   uint32_t partial = NIL, hit = NIL, reuse = 0, hit_idx = NIL;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
@@ -1020,7 +1020,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     const uint32_t cmp = min(len, n - pos);
     const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, off + pos, cmp);
     if (lane == 0 && npath >= 32) C.w.path()[npath] = c;
-    if (lane == npath) my_path = c;
+    if (lane == npath) { my_path = c; my_ds = pos; my_de = de; my_fl = fl; }
     npath++;
     pinned_bytes += node_bytes(C.m, pos, de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
@@ -1094,6 +1094,41 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
       p = m_in;
       p_gain = v;
     }
+  }
+  // Chunked state passing (NEXT-3): the prefill checkpoint moves down to the
+  // chunk boundary at or below the branch point; skipped if that is 0 or not beyond the hit.
+  if (C.chunk && p) {
+    uint32_t pa = (p / C.chunk) * C.chunk;
+    if (pa == 0 || pa <= reuse) pa = 0;
+    p_split = NIL;
+    p_gain = NIL;
+    if (pa) {
+      const bool mine = lane < min(npath, 32u);
+      const unsigned bnd = __ballot_sync(FULL, mine && my_de == pa && my_path != partial);
+      const unsigned ins = __ballot_sync(FULL, mine && my_ds < pa && pa < my_de);
+      if (bnd) {
+        const int src = __ffs(bnd) - 1;
+        const uint32_t x = __shfl_sync(FULL, my_path, src);
+        if (__shfl_sync(FULL, my_fl, src) & F_SSM) pa = 0; else p_gain = x;
+      } else if (ins) {
+        p_split = __shfl_sync(FULL, my_path, __ffs(ins) - 1);
+      } else {  // deeper than 32 levels: scan the spilled part of the path
+        uint32_t kind = 0, x = NIL;
+        if (lane == 0)
+          for (uint32_t i = 32; i < npath; i++) {
+            const uint32_t y = C.w.path()[i];
+            const NodeRec Ry = C.w.rec()[y];
+            if (y != partial && Ry.de == pa) { kind = ((Ry.nf >> 24) & F_SSM) ? 3 : 1; x = y; break; }
+            if (Ry.ds < pa && pa < Ry.de) { kind = 2; x = y; break; }
+          }
+        kind = __shfl_sync(FULL, kind, 0);
+        x = __shfl_sync(FULL, x, 0);
+        if (kind == 1) p_gain = x;
+        else if (kind == 2) p_split = x;
+        else pa = 0;
+      }
+    }
+    p = pa;
   }
   // Step 4: plan -- checkpoints {p, n}, at most two.
   const bool leaf = m < n;
@@ -1197,6 +1232,7 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.m = V.m;
   C.capb = V.cap_bytes;
   C.capn = V.cap_nodes;
+  C.chunk = V.chunk;
   C.alpha = alpha;
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;

@@ -1,5 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for f in build/variants/*.so; do
-  MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -1
-done | tee gpurun_out/variants.txt
+timeout 1800 python -m pytest tests -m gpu -x -q --durations=5 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -25 gpurun_out/pytest_gpu.log

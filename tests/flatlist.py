@@ -58,7 +58,8 @@ def _lcp(a, b) -> int:
 
 class FlatCache:
     def __init__(self, model, cap_bytes: int, cap_nodes: int = 0, alpha: float = 0.0,
-                 policy="marconi"):
+                 policy="marconi", chunk: int = 0):
+        self.chunk = chunk
         self.m = model
         self.cap_bytes = cap_bytes
         self.cap_nodes = cap_nodes
@@ -134,13 +135,26 @@ class FlatCache:
         P = full + ([partial] if partial else [])
         # speculative insertion with the c.3 #8/#9 readings
         m_in = min(m, L_in)
-        p, p_split, p_gain = 0, False, None
+        q = 0
         if m_in > 0:
             b = self.at(S, m_in)
+            if b is None or not b.has_ssm:
+                q = m_in
+        # chunked state passing: checkpoint at the chunk boundary <= q
+        p = q
+        if q and self.chunk:
+            p = (q // self.chunk) * self.chunk
+            if p == 0 or p <= reuse:
+                p = 0
+        p_split, p_gain = False, None
+        if p:
+            b = self.at(S, p)
             if b is None:
-                p, p_split = m_in, True
+                p_split = True
             elif not b.has_ssm:
-                p, p_gain = m_in, b
+                p_gain = b
+            else:
+                p = 0
         splits = []
         if p_split:
             splits.append((p, True))
@@ -217,8 +231,8 @@ class FlatCache:
         return out
 
 
-def replay(trace, model, cap_bytes, cap_nodes, alpha, policy="marconi"):
-    c = FlatCache(model, cap_bytes, cap_nodes, alpha, policy)
+def replay(trace, model, cap_bytes, cap_nodes, alpha, policy="marconi", chunk=0):
+    c = FlatCache(model, cap_bytes, cap_nodes, alpha, policy, chunk)
     res = []
     for r in range(1, trace.n_requests + 1):
         s = trace.seq(r)

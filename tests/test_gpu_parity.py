@@ -378,3 +378,51 @@ def test_errors_are_loud():
         ctx2.replay([-1.0])
     with pytest.raises(M.MarconiError):
         M.Context([tg.Variant(tg.Model(0, 4, 4), 10)], max_nodes=64)
+
+
+# ---------------------------------------------------------------- NEXT-3: chunk-aligned checkpoints
+def test_chunked_paper_example_on_gpu():
+    """branch at 80, chunk 32 -> the state is checkpointed at 64."""
+    A = list(range(1, 81))
+    reqs = [(A + [500 + j for j in range(20)], []), (A + [600 + j for j in range(20)], []),
+            (A + [700 + j for j in range(20)], [])]
+    tr = tg.from_sequences(reqs)
+    for chunk, want in ((32, [0, 0, 64]), (0, [0, 0, 80]), (128, [0, 0, 0])):
+        v = tg.Variant(tg.MODEL_7B, tg.UNLIMITED_BYTES, 0, chunk)
+        g, out = GU.gpu_grid(tr, [v], [0.0], 1, max_nodes=64)
+        assert out["hit"].cpu().numpy()[0, 0].tolist() == want, chunk
+
+
+def test_chunked_micro_traces():
+    for chunk in (2, 3, 8):
+        for seed in range(60):
+            tr = tg.micro_trace(seed, n_req=20, max_len=64, alphabet=2 + seed % 3)
+            v = tg.Variant(tg.MODEL_7B, tg.UNLIMITED_BYTES, 2 + seed % 6, chunk)
+            alphas = [0.0, tg.ALPHA_GRID16[seed % 16]]
+            g, out = GU.gpu_grid(tr, [v], alphas, 2, max_nodes=128, log_cap=256)
+            snaps, live, res, segs = GU.oracle_grid(tr, [v], alphas, 2, threads=1)
+            for k in range(len(snaps[0])):
+                gs, gn = g.ctx.get_snapshot(0, k)
+                assert gn == snaps[0][k][1] and np.array_equal(GU.canon(gs), GU.canon(snaps[0][k][0]))
+            hit = out["hit"].cpu().numpy()
+            for cid, (h, f, b, c) in res.items():
+                ai, si = cid // len(segs), cid % len(segs)
+                first, n, k = segs[si]
+                assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h), (chunk, seed, cid)
+                _, _, _, lg = GU.oracle_chain_log(tr, v, alphas[ai], first, n, snaps[0][k])
+                glog, gn = g.ctx.read_log(out, cid)
+                _assert_logs_equal(glog, gn, lg, f"chunk {chunk} seed {seed}")
+
+
+@pytest.mark.parametrize("chunk", [32, 256])
+def test_chunked_config3_reduced(chunk):
+    w = tg.workload(3, R=6000)
+    w.variants = [tg.Variant(tg.MODEL_7B, 60 * tg.GB, 0, chunk)]
+    w.n_segments = 12
+    _compare_grid(w)
+
+
+def test_chunked_config4_full():
+    w = tg.workload(4)
+    w.variants = [tg.Variant(tg.MODEL_7B, 60 * tg.GB, 0, 64)]
+    _compare_grid(w)

@@ -126,6 +126,7 @@ class Variant:
     model: Model
     capacity_bytes: int
     capacity_nodes: int = 0
+    chunk_size: int = 0  # 0 = exact checkpoints; else chunk-aligned prefill checkpoints (NEXT-3)
 
 
 @dataclasses.dataclass
