@@ -426,3 +426,21 @@ def test_chunked_config4_full():
     w = tg.workload(4)
     w.variants = [tg.Variant(tg.MODEL_7B, 60 * tg.GB, 0, 64)]
     _compare_grid(w)
+
+
+# ---------------------------------------------------------------- NEXT-4: sweeps on the same kernels
+def test_state_dim_sweep():
+    """fig:microbenchmark_state_dim axis: N in {16, 32, 64, 128} as 4 cache variants
+    of one grid (one context, one launch), every chain vs the oracle."""
+    w = tg.workload(3, R=5000)
+    w.variants = tg.state_dim_variants()
+    w.alphas = (0.0, 1 / 16, 1.0, 16.0)
+    w.n_segments = 10
+    _compare_grid(w)
+
+
+@pytest.mark.parametrize("rate,delay", [(0.5, 5.0), (2.0, 5.0), (1.0, 10.0)])
+def test_arrival_sweep(rate, delay):
+    """fig:micro_arrival axes: session rate 0.5 -> 2 /s, response time 5 -> 10 s."""
+    w = tg.arrival_workload(rate, delay, R=6000, n_segments=12, alphas=(0.0, 0.25, 4.0))
+    _compare_grid(w)

@@ -25,6 +25,7 @@ def test_spec_layer_goldens():
     assert t["ssm_state_bytes"] == 1_048_576
     assert t["conv_state_bytes"] == 67_584
     assert O.layer_terms(M, 16)["kv_bytes"] == 262_144      # SPEC:89 (linearity)
+    assert O.layer_terms(tg.Model(4, 24, 28, d_state=16), 1)["ssm_state_bytes"] == 131_072  # SPEC:98, N=16 axis
     z = O.layer_terms(M, 0)
     assert z["attention_flops"] == z["ssm_flops"] == z["mlp_flops"] == z["kv_bytes"] == 0
 

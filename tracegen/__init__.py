@@ -498,3 +498,23 @@ def workload(cfg: int, R: Optional[int] = None, problem: int = 0) -> Workload:
               for c in (60, 80, 100, 120, 140)]
         return Workload("synthetic", tr, vs, ALPHA_GRID16, 16)
     raise ValueError(f"unknown config {cfg}")
+
+
+# ----------------------------------------------------------------------------
+# NEXT-4 sweeps (same kernels, second workloads): SSM state dimension N
+# (fig:microbenchmark_state_dim) and session / request arrival rates
+# (fig:micro_arrival).
+# ----------------------------------------------------------------------------
+def state_dim_variants(capacity_bytes: int = 60 * GB, dims=(16, 32, 64, 128)) -> List[Variant]:
+    """7B hybrid {4,24,28} with d_state N in dims (conv_in = 2D + 2N follows N)."""
+    return [Variant(Model(4, 24, 28, 4096, n, 2, 2 * 4096 + 2 * n, 4), capacity_bytes) for n in dims]
+
+
+def arrival_workload(session_rate: float, mean_delay: float, R: int = 20_000, n_segments: int = 32,
+                     alphas=ALPHA_GRID16) -> Workload:
+    """ShareGPT-shaped trace with the given session arrival rate (sessions/s) and mean
+    inter-request delay within a session (s) -- the two axes of fig:micro_arrival."""
+    seed = 2000 + int(session_rate * 100) + int(mean_delay * 10)
+    tr = gen_trace(f"sharegpt_rate{session_rate}_delay{mean_delay}", R, seed, session_rate,
+                   [("sharegpt", 1.0)], mean_delay=mean_delay)
+    return Workload(tr.name, tr, [Variant(MODEL_7B, 60 * GB)], tuple(alphas), n_segments)
