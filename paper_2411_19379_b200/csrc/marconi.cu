@@ -39,7 +39,10 @@ mc_status fail(mc_status s, const std::string& m) {
 #ifndef MC_MINBLOCKS
 #define MC_MINBLOCKS 4
 #endif
-constexpr int kWarpsPerCta = 4;
+#ifndef MC_WARPS_PER_CTA
+#define MC_WARPS_PER_CTA 4
+#endif
+constexpr int kWarpsPerCta = MC_WARPS_PER_CTA;
 }  // namespace
 
 // ---------------------------------------------------------------------------
