@@ -98,7 +98,7 @@ struct __align__(8) DenseRec {  // one dense position: the scanned key pair
 };
 
 struct __align__(16) NodeRec {
-  uint32_t parent, ftok, ds, de;  // first 16 B: what the child index reads
+  uint32_t parent, hidx, ds, de;  // hidx = position of the node's own entry in the child index
   uint32_t roff, cxor, nf, dpos;  // roff = pool offset of the node's request; nf = nchild | flags << 24
 };
 
@@ -346,10 +346,11 @@ __device__ __forceinline__ uint32_t hash_index_1(const Chain& C, uint32_t parent
     i = (i + 1) & C.hmask;
   }
 }
-__device__ __forceinline__ void hash_insert_1(Chain& C, const HEnt& ne, uint32_t parent) {
+__device__ __forceinline__ uint32_t hash_insert_1(Chain& C, const HEnt& ne, uint32_t parent) {
   uint32_t i = hslot(parent, ne.tok, C.hmask);
   while (hvalid(C, C.w.tab()[i].key)) i = (i + 1) & C.hmask;
   C.w.tab()[i] = ne;
+  return i;
 }
 __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
   uint32_t j = i;
@@ -361,6 +362,7 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
     const bool stays = (i <= j) ? (i < home && home <= j) : (i < home || home <= j);
     if (!stays) {
       C.w.tab()[i] = e;
+      C.w.rec()[e.key & SLOT14].hidx = i;  // the moved entry's node keeps knowing its position
       i = j;
     }
   }
@@ -447,7 +449,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   __syncwarp();
   if (lane == 0) {
     NodeRec z;
-    z.parent = NIL; z.ftok = 0; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
+    z.parent = NIL; z.hidx = NIL; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
     C.w.rec()[0] = z;
   }
   uint64_t bytes = 0;
@@ -459,7 +461,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     bad |= (r.d_end <= r.d_start) || (r.ref_off + r.d_end > P.n_tok) || (pi != NIL && pi >= n);
     NodeRec R;
     R.parent = (pi == NIL) ? 0u : pi + 1;
-    R.ftok = P.tok[r.ref_off + r.d_start];
+    R.hidx = NIL;
     R.ds = r.d_start;
     R.de = r.d_end;
     R.roff = (uint32_t)r.ref_off;
@@ -475,7 +477,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec& R = C.w.rec()[s];
-    const uint32_t ps = R.parent, ft = R.ftok;
+    const uint32_t ps = R.parent, ft = P.tok[(uint64_t)R.roff + R.ds];
     atomicAdd(&C.w.rec()[ps].nf, 1u);
     atomicXor(&C.w.rec()[ps].cxor, s);
     uint32_t j = hslot(ps, ft, C.hmask);
@@ -485,6 +487,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
       if (hvalid(C, k)) { j = (j + 1) & C.hmask; continue; }
       if (atomicCAS(&C.w.tab()[j].key, k, nk) == k) break;
     }
+    C.w.rec()[s].hidx = j;
     HEnt& E = C.w.tab()[j];
     E.tok = ft;
     E.de = R.de | (((R.nf >> 24) & F_SSM) ? 0x80000000u : 0u);
@@ -866,9 +869,8 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     double e_moved = e_last;
     if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
       kind = 0;
-      const uint32_t hx = hash_index_1(C, p, X.ftok);
       C.total -= node_bytes(C.m, X.ds, X.de, xf & F_SSM);
-      hash_erase_at_1(C, hx);
+      hash_erase_at_1(C, X.hidx);
       NodeRec& Wp = C.w.rec()[p];
       Wp.nf = Rp.nf - 1;
       Wp.cxor = Rp.cxor ^ x;
@@ -878,14 +880,15 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       kind = 1;
       const uint32_t c = X.cxor;
       const NodeRec Rc = C.w.rec()[c];
-      const uint32_t hc = hash_index_1(C, x, Rc.ftok);  // entry of c under x (erased)
-      const uint32_t hx = hash_index_1(C, p, X.ftok);   // entry of x under p (now c's)
+      const uint32_t hc = Rc.hidx;   // entry of c under x (erased)
+      const uint32_t hx = X.hidx;    // entry of x under p (becomes c's: same key)
+      const uint32_t xtok = C.w.tab()[hx].tok;
       if (xf & F_SSM) C.total -= C.m.ssmb;
       NodeRec& Wc = C.w.rec()[c];
-      Wc.ds = X.ds;          // c's key becomes (p, first token of x) -- same home as hx
-      Wc.ftok = X.ftok;
+      Wc.ds = X.ds;
       Wc.parent = p;
-      C.w.tab()[hx] = hmake(C, p, X.ftok, c, Rc.de, (Rc.nf >> 24) & F_SSM, Rc.roff);
+      Wc.hidx = hx;
+      C.w.tab()[hx] = hmake(C, p, xtok, c, Rc.de, (Rc.nf >> 24) & F_SSM, Rc.roff);
       hash_erase_at_1(C, hc);
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
       const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
@@ -929,18 +932,18 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   const NodeRec Y = C.w.rec()[y];
   const uint32_t cx = C.w.rec()[Y.parent].cxor;
   const uint32_t ft = P.tok[(uint64_t)Y.roff + x];
-  const uint32_t hi = hash_index_1(C, Y.parent, Y.ftok);  // entry of y under its parent
+  const uint32_t hi = Y.hidx;                  // entry of y under its parent
+  const uint32_t ytok = C.w.tab()[hi].tok;
   NodeRec U;
-  U.parent = Y.parent; U.ftok = Y.ftok; U.ds = Y.ds; U.de = x;
+  U.parent = Y.parent; U.hidx = hi; U.ds = Y.ds; U.de = x;
   U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
   C.w.rec()[u] = U;
   C.w.ids()[u] = C.next_id++;
-  C.w.tab()[hi] = hmake(C, Y.parent, Y.ftok, u, x, stateful, Y.roff);  // same key, new child
+  C.w.tab()[hi] = hmake(C, Y.parent, ytok, u, x, stateful, Y.roff);  // same key, new child
   NodeRec& Ry = C.w.rec()[y];
   Ry.parent = u;
   Ry.ds = x;
-  Ry.ftok = ft;
-  hash_insert_1(C, hmake(C, u, ft, y, Y.de, (Y.nf >> 24) & F_SSM, Y.roff), u);
+  Ry.hidx = hash_insert_1(C, hmake(C, u, ft, y, Y.de, (Y.nf >> 24) & F_SSM, Y.roff), u);
   C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
   d_set_eff(C, Y.dpos, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
@@ -950,8 +953,7 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   NodeRec& R = C.w.rec()[x];
-  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de, pa = R.parent, ft = R.ftok;
-  const uint32_t hi = hash_index_1(C, pa, ft);
+  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de, hi = R.hidx;
   R.nf = nf | (F_SSM << 24);
   C.w.tab()[hi].de = de | 0x80000000u;  // the child index carries the state flag for the walk
   d_set_eff(C, dp, node_eff(C.m, ds, de, true));
@@ -1169,11 +1171,11 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
           const uint32_t ft = P.tok[off + m];
           const NodeRec Ra = C.w.rec()[attach];
           NodeRec W;
-          W.parent = attach; W.ftok = ft; W.ds = m; W.de = n;
+          W.parent = attach; W.hidx = NIL; W.ds = m; W.de = n;
           W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
           C.w.rec()[w] = W;
           C.w.ids()[w] = C.next_id++;
-          hash_insert_1(C, hmake(C, attach, ft, w, n, true, (uint32_t)off), attach);
+          C.w.rec()[w].hidx = hash_insert_1(C, hmake(C, attach, ft, w, n, true, (uint32_t)off), attach);
           NodeRec& Wa = C.w.rec()[attach];
           Wa.nf = Ra.nf + 1;
           Wa.cxor = Ra.cxor ^ w;

@@ -1,7 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+for i in 1 2; do
 for f in build/variants/*.so; do
   MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -1
-done | tee gpurun_out/variants.txt
-MAXN=4096 MARCONI_LIB=$PWD/build/variants/lib_u2.so timeout 300 python tools/variant_timing.py 2>&1 | tail -1 | sed 's/^/maxn4096 /'
-MAXN=2048 MARCONI_LIB=$PWD/build/variants/lib_u2.so timeout 300 python tools/variant_timing.py 2>&1 | tail -1 | sed 's/^/maxn2048 /'
+done; done | tee gpurun_out/variants.txt
