@@ -260,6 +260,10 @@ struct Chain {
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
   uint32_t moved_slot, moved_pos;  // last eviction: node whose dense entry moved, and where
+  // cached normalisation bounds (exact when bc_valid): adds extend them, removing or
+  // changing a node that holds an extreme invalidates them (pass 1 then recomputes)
+  uint32_t bc_valid, bc_tmin, bc_tmax;
+  float bc_lo, bc_hi;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   unsigned long long t_walk, t_evict, t_insert, t_unpin;
 #endif
@@ -277,6 +281,11 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.failed = __shfl_sync(FULL, (int)C.failed, 0);
   C.moved_slot = __shfl_sync(FULL, C.moved_slot, 0);
   C.moved_pos = __shfl_sync(FULL, C.moved_pos, 0);
+  C.bc_valid = __shfl_sync(FULL, C.bc_valid, 0);
+  C.bc_tmin = __shfl_sync(FULL, C.bc_tmin, 0);
+  C.bc_tmax = __shfl_sync(FULL, C.bc_tmax, 0);
+  C.bc_lo = __shfl_sync(FULL, C.bc_lo, 0);
+  C.bc_hi = __shfl_sync(FULL, C.bc_hi, 0);
 }
 
 __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_t mask) {
@@ -378,13 +387,37 @@ __device__ __forceinline__ uint32_t d_slot(const Chain& C, uint32_t i) { return 
 __device__ __forceinline__ void d_set_slot(Chain& C, uint32_t i, uint32_t s) { C.w.dslot()[i] = s; }
 __device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[d_slot(C, i)]; }
 __device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
+// bound-cache hooks (lane 0, or uniform)
+__device__ __forceinline__ void bc_add(Chain& C, uint32_t t, float e) {
+  C.bc_tmin = min(C.bc_tmin, t);
+  C.bc_tmax = max(C.bc_tmax, t);
+  C.bc_lo = fminf(C.bc_lo, e);
+  C.bc_hi = fmaxf(C.bc_hi, e);
+}
+__device__ __forceinline__ void bc_change_e(Chain& C, float old_e, float new_e) {
+  if (old_e == C.bc_lo || old_e == C.bc_hi) C.bc_valid = 0;
+  C.bc_lo = fminf(C.bc_lo, new_e);
+  C.bc_hi = fmaxf(C.bc_hi, new_e);
+}
+__device__ __forceinline__ void bc_change_t(Chain& C, uint32_t old_t, uint32_t new_t) {
+  if (old_t == C.bc_tmin) C.bc_valid = 0;
+  C.bc_tmax = max(C.bc_tmax, new_t);
+}
+__device__ __forceinline__ void bc_remove(Chain& C, uint32_t t, float e) {
+  if (t == C.bc_tmin || t == C.bc_tmax || e == C.bc_lo || e == C.bc_hi) C.bc_valid = 0;
+}
+// eff of an EXISTING dense position changes
 __device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
   C.w.eff64()[i] = v;
-  d_ptr(C, i)->e32 = __double2float_rn(v);
+  DenseRec* d = d_ptr(C, i);
+  const float e = __double2float_rn(v);
+  bc_change_e(C, d->e32, e);
+  d->e32 = e;
 }
 // (re)stamp dense position i with timestamp t, keeping its flags (lane 0)
 __device__ __forceinline__ void d_stamp(Chain& C, uint32_t i, uint32_t t) {
   DenseRec* d = d_ptr(C, i);
+  bc_change_t(C, d->tc & T_MASK, t);
   d->tc = t | (d->tc & D_FLAGS);
 }
 __device__ __forceinline__ void d_multi(Chain& C, uint32_t i, uint32_t nchild) {
@@ -396,8 +429,12 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   NodeRec& R = C.w.rec()[s];
   R.dpos = i;
   d_set_slot(C, i, s);
-  d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
-  d_set_tc(C, i, t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u));
+  const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
+  C.w.eff64()[i] = v;
+  DenseRec* d = d_ptr(C, i);
+  d->e32 = __double2float_rn(v);
+  d->tc = t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u);
+  bc_add(C, t, d->e32);
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
   if (C.nfree) return C.w.freel()[--C.nfree];
@@ -497,8 +534,11 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
-    d_set_tc(C, i, nodes[i].t_last | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u));
-    d_set_eff(C, i, node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM));
+    const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
+    C.w.eff64()[i] = v;
+    DenseRec* d = d_ptr(C, i);
+    d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u);
+    d->e32 = __double2float_rn(v);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(FULL, (unsigned long long)bytes, o);
@@ -511,6 +551,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   C.next_id = nid;
   C.hwm = n + 1;
   C.nfree = 0;
+  C.bc_valid = 0;
   __syncwarp();
 }
 
@@ -710,7 +751,13 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
 #else
 #define T3(ctr) do {} while (0)
 #endif
-  // pass 1: exact t bounds, fp32 eff bounds over ALL non-root nodes (R1)
+  // pass 1: exact t bounds, fp32 eff bounds over ALL non-root nodes (R1) -- skipped when
+  // the cached bounds are known exact
+  uint32_t tmin, tmax;
+  float lo32, hi32;
+  if (C.bc_valid) {
+    tmin = C.bc_tmin; tmax = C.bc_tmax; lo32 = C.bc_lo; hi32 = C.bc_hi;
+  } else {
   uint32_t tmn[kUnroll], tmx[kUnroll];
   float lo[kUnroll], hi[kUnroll];
 #pragma unroll
@@ -724,8 +771,8 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     lo[q] = fminf(lo[q], e);
     hi[q] = fmaxf(hi[q], e);
   });
-  uint32_t tmin = tmn[0], tmax = tmx[0];
-  float lo32 = lo[0], hi32 = hi[0];
+  tmin = tmn[0]; tmax = tmx[0];
+  lo32 = lo[0]; hi32 = hi[0];
 #pragma unroll
   for (int q = 1; q < kUnroll; q++) {
     tmin = min(tmin, tmn[q]); tmax = max(tmax, tmx[q]); lo32 = fminf(lo32, lo[q]); hi32 = fmaxf(hi32, hi[q]);
@@ -736,6 +783,12 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     tmax = max(tmax, __shfl_xor_sync(FULL, tmax, o));
     lo32 = fminf(lo32, __shfl_xor_sync(FULL, lo32, o));
     hi32 = fmaxf(hi32, __shfl_xor_sync(FULL, hi32, o));
+  }
+  Chain& Cw = const_cast<Chain&>(C);
+  Cw.bc_valid = 1; Cw.bc_tmin = tmin; Cw.bc_tmax = tmax; Cw.bc_lo = lo32; Cw.bc_hi = hi32;
+#ifdef MC_PHASE_TIMERS3
+  CC.t_insert += 1ull << 32;  // count full bound passes (high half)
+#endif
   }
   b.tmin = tmin;
   b.tmax = tmax;
@@ -907,6 +960,10 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     }
     // dense_remove: move the last dense entry into the victim's position
     const uint32_t i = X.dpos;
+    {
+      const DenseRec dv = *d_ptr(C, i);
+      bc_remove(C, dv.tc & T_MASK, dv.e32);
+    }
     C.moved_slot = NIL;
     if (i != last) {
       C.moved_slot = sl;
@@ -1063,19 +1120,25 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
 
   // Pin the path (R12) and touch only the hit node (step 5): every path
   // lane reads its node's dense position and updates its dense word in parallel.
-  uint32_t my_dp = NIL;
+  uint32_t my_dp = NIL, old_t = 0;
   if (lane < min(npath, 32u)) {
     my_dp = C.w.rec()[my_path].dpos;
     DenseRec* d = d_ptr(C, my_dp);
     const uint32_t tc = d->tc;
+    if (lane == hit_idx) old_t = tc & T_MASK;
     d->tc = (lane == hit_idx ? (r | (tc & D_MULTI)) : tc) | D_PIN;
   }
   if (lane == 0)
     for (uint32_t i = 32; i < npath; i++) {
       DenseRec* d = d_ptr(C, C.w.rec()[C.w.path()[i]].dpos);
+      if (i == hit_idx) old_t = d->tc & T_MASK;
       d->tc = (i == hit_idx ? (r | (d->tc & D_MULTI)) : d->tc) | D_PIN;
     }
-  if (hit != NIL) C.c_wr += 1;
+  if (hit != NIL) {
+    C.c_wr += 1;
+    old_t = __shfl_sync(FULL, old_t, hit_idx < 32 ? hit_idx : 0);
+    bc_change_t(C, old_t, r);  // uniform: every lane updates its copy of the bound cache
+  }
   __syncwarp();
 
   // Step 3: speculative insertion of the input (R8, R9).
@@ -1240,6 +1303,8 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.n_evict = 0;
   C.moved_slot = NIL;
   C.moved_pos = 0;
+  C.bc_valid = 0;
+  C.bc_tmin = 0; C.bc_tmax = 0; C.bc_lo = 0.0f; C.bc_hi = 0.0f;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   C.t_walk = C.t_evict = C.t_insert = C.t_unpin = 0;
 #endif

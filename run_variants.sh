@@ -4,5 +4,5 @@ timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 tail -3 gpurun_out/pytest_gpu.log
 for i in 1 2; do
 for f in build/variants/*.so; do
-  MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -1
+  PHASES3=1 MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -3
 done; done | tee gpurun_out/variants.txt

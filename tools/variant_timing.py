@@ -38,3 +38,6 @@ if os.environ.get("PHASES3"):
     nreq = len(g.chains) * w.window
     print("per request k-cycles: pass1 %.1f pass2 %.1f verify %.1f ; fallbacks per request %.4f" %
           (tot[0] / nreq / 1e3, tot[1] / nreq / 1e3, tot[2] / nreq / 1e3, tot[3] / nreq))
+if os.environ.get("PHASES3"):
+    tot_pass1 = (ctr[:, 2].astype(np.uint64) >> np.uint64(32)).sum()
+    print("full bound passes (pass 1) per request: %.3f" % (float(tot_pass1) / (len(g.chains) * w.window)))
