@@ -262,8 +262,11 @@ struct Chain {
   uint32_t moved_slot, moved_pos;  // last eviction: node whose dense entry moved, and where
   // cached normalisation bounds (exact when bc_valid): adds extend them, removing or
   // changing a node that holds an extreme invalidates them (pass 1 then recomputes)
+  // (bc_elo/bc_ehi: the exact fp64 extremes; bc_lo/bc_hi = their RN32 images, which are
+  // the fp32 extremes because RN is monotone)
   uint32_t bc_valid, bc_tmin, bc_tmax;
   float bc_lo, bc_hi;
+  double bc_elo, bc_ehi;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   unsigned long long t_walk, t_evict, t_insert, t_unpin;
 #endif
@@ -286,6 +289,8 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.bc_tmax = __shfl_sync(FULL, C.bc_tmax, 0);
   C.bc_lo = __shfl_sync(FULL, C.bc_lo, 0);
   C.bc_hi = __shfl_sync(FULL, C.bc_hi, 0);
+  C.bc_elo = __shfl_sync(FULL, C.bc_elo, 0);
+  C.bc_ehi = __shfl_sync(FULL, C.bc_ehi, 0);
 }
 
 __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_t mask) {
@@ -388,16 +393,18 @@ __device__ __forceinline__ void d_set_slot(Chain& C, uint32_t i, uint32_t s) { C
 __device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[d_slot(C, i)]; }
 __device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
 // bound-cache hooks (lane 0, or uniform)
-__device__ __forceinline__ void bc_add(Chain& C, uint32_t t, float e) {
+__device__ __forceinline__ void bc_extend_e(Chain& C, float e32, double e64) {
+  if (e64 < C.bc_elo) { C.bc_elo = e64; C.bc_lo = e32; }
+  if (e64 > C.bc_ehi) { C.bc_ehi = e64; C.bc_hi = e32; }
+}
+__device__ __forceinline__ void bc_add(Chain& C, uint32_t t, float e32, double e64) {
   C.bc_tmin = min(C.bc_tmin, t);
   C.bc_tmax = max(C.bc_tmax, t);
-  C.bc_lo = fminf(C.bc_lo, e);
-  C.bc_hi = fmaxf(C.bc_hi, e);
+  bc_extend_e(C, e32, e64);
 }
-__device__ __forceinline__ void bc_change_e(Chain& C, float old_e, float new_e) {
+__device__ __forceinline__ void bc_change_e(Chain& C, float old_e, float new_e32, double new_e64) {
   if (old_e == C.bc_lo || old_e == C.bc_hi) C.bc_valid = 0;
-  C.bc_lo = fminf(C.bc_lo, new_e);
-  C.bc_hi = fmaxf(C.bc_hi, new_e);
+  bc_extend_e(C, new_e32, new_e64);
 }
 __device__ __forceinline__ void bc_change_t(Chain& C, uint32_t old_t, uint32_t new_t) {
   if (old_t == C.bc_tmin) C.bc_valid = 0;
@@ -411,7 +418,7 @@ __device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
   C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
   const float e = __double2float_rn(v);
-  bc_change_e(C, d->e32, e);
+  bc_change_e(C, d->e32, e, v);
   d->e32 = e;
 }
 // (re)stamp dense position i with timestamp t, keeping its flags (lane 0)
@@ -434,7 +441,7 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   DenseRec* d = d_ptr(C, i);
   d->e32 = __double2float_rn(v);
   d->tc = t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u);
-  bc_add(C, t, d->e32);
+  bc_add(C, t, d->e32, v);
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
   if (C.nfree) return C.w.freel()[--C.nfree];
@@ -593,17 +600,21 @@ __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, 
                                               uint32_t cmp) {
   if (a == b) return cmp;  // same pool range: identical tokens
   const uint32_t lane = lane_id();
-  for (uint32_t base = 0; base < cmp; base += 128) {
-    unsigned mis[4];
+#ifndef MC_MATCH_BLOCKS
+#define MC_MATCH_BLOCKS 4
+#endif
+  constexpr int kB = MC_MATCH_BLOCKS;  // 32-token blocks compared per round trip
+  for (uint32_t base = 0; base < cmp; base += 32 * kB) {
+    unsigned mis[kB];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < kB; q++) {
       const uint32_t j = base + 32 * q + lane;
       bool bad = false;
       if (j < cmp) bad = __ldg(tok + a + j) != __ldg(tok + b + j);
       mis[q] = __ballot_sync(FULL, bad);
     }
 #pragma unroll
-    for (int q = 0; q < 4; q++)
+    for (int q = 0; q < kB; q++)
       if (mis[q]) return base + 32 * q + (__ffs(mis[q]) - 1);
   }
   return cmp;
@@ -757,6 +768,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   float lo32, hi32;
   if (C.bc_valid) {
     tmin = C.bc_tmin; tmax = C.bc_tmax; lo32 = C.bc_lo; hi32 = C.bc_hi;
+    b.emin = C.bc_elo; b.emax = C.bc_ehi;
   } else {
   uint32_t tmn[kUnroll], tmx[kUnroll];
   float lo[kUnroll], hi[kUnroll];
@@ -784,15 +796,28 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     lo32 = fminf(lo32, __shfl_xor_sync(FULL, lo32, o));
     hi32 = fmaxf(hi32, __shfl_xor_sync(FULL, hi32, o));
   }
+  // exact fp64 extremes: the fp64 values of the entries holding the fp32 extremes
+  double2 ex = recover_extremes(C.sd, C.w.tail(), C.w.eff64(), cnt, C.S, lo32, hi32);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double xl = __shfl_xor_sync(FULL, ex.x, o), xh = __shfl_xor_sync(FULL, ex.y, o);
+    ex.x = xl < ex.x ? xl : ex.x;
+    ex.y = xh > ex.y ? xh : ex.y;
+  }
+  b.emin = ex.x;
+  b.emax = ex.y;
   Chain& Cw = const_cast<Chain&>(C);
   Cw.bc_valid = 1; Cw.bc_tmin = tmin; Cw.bc_tmax = tmax; Cw.bc_lo = lo32; Cw.bc_hi = hi32;
+  Cw.bc_elo = ex.x; Cw.bc_ehi = ex.y;
 #ifdef MC_PHASE_TIMERS3
-  CC.t_insert += 1ull << 32;  // count full bound passes (high half)
+  CC.t_unpin += 1ull << 32;  // count full bound passes (high half)
 #endif
   }
   b.tmin = tmin;
   b.tmax = tmax;
-  T3(t_walk);
+#ifdef MC_PHASE_TIMERS3
+  _t3 = clock64();
+#endif
   // pass 2: fp32 filter keys, best two per lane (branch-free), exact fp64 extremes
   const bool dt0 = tmax == tmin;
   const double de32 = (double)hi32 - (double)lo32;  // exact in fp64
@@ -804,22 +829,13 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   uint32_t ai[kUnroll];
 #pragma unroll
   for (int q = 0; q < kUnroll; q++) { a1[q] = INF; a2[q] = INF; ai[q] = NIL; }
-  uint32_t ilo = NIL, ihi = NIL, nlo = 0, nhi = 0;
-  const float dmin = __uint2float_rn(tmin);
   scan_dense(C, cnt, [&](int q, uint32_t i, uint32_t tc, float e) {
-    // entries holding the fp32 extremes (their fp64 values decide the exact bounds)
-    const bool el = e == lo32, eh = e == hi32;
-    ilo = el ? i : ilo;
-    nlo += el;
-    ihi = eh ? i : ihi;
-    nhi += eh;
     const float k = (tc & D_FLAGS) ? INF : __fmaf_rn(__fsub_rn(e, lo32), aide, __fmul_rn(__uint2float_rn(tc - tmin), idt));
     const bool lt1 = k < a1[q], lt2 = k < a2[q];
     a2[q] = lt1 ? a1[q] : (lt2 ? k : a2[q]);
     ai[q] = lt1 ? i : ai[q];
     a1[q] = lt1 ? k : a1[q];
   });
-  (void)dmin;
   // merge the per-slot best-two lists
   float k1 = a1[0], k2 = a2[0];
   uint32_t i1 = ai[0];
@@ -830,29 +846,11 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   }
   // issue the fp64 reads this lane may need (extremes, its best candidate) before the
   // warp reductions so their latency overlaps the shuffles
-  const double pre_lo = (nlo == 1) ? e64[ilo] : 0.0;
-  const double pre_hi = (nhi == 1) ? e64[ihi] : 0.0;
   const double pre_k1 = (i1 != NIL) ? e64[i1] : 0.0;
   const uint32_t pre_slot = (i1 != NIL) ? d_slot(C, i1) : NIL;
-  double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
-  if (__any_sync(FULL, nlo > 1 || nhi > 1)) {
-    // several entries share an fp32 extreme: read all of their fp64 values (cold path)
-    const double2 ex = recover_extremes(C.sd, C.w.tail(), e64, cnt, C.S, lo32, hi32);
-    elo = ex.x;
-    ehi = ex.y;
-  } else {
-    if (nlo) elo = pre_lo;
-    if (nhi) ehi = pre_hi;
-  }
   float kmin = k1;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
-    elo = fmin(elo, __shfl_xor_sync(FULL, elo, o));
-    ehi = fmax(ehi, __shfl_xor_sync(FULL, ehi, o));
-  }
-  b.emin = elo;
-  b.emax = ehi;
+  for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
   T3(t_evict);
   if (kmin == INF) return best;  // no candidate
   // δ = 2^-19 (1 + α (1 + 4 emax/Δe32)); a zero fp32 range cannot resolve eff -> exact pass
@@ -879,12 +877,10 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.i = __shfl_sync(FULL, best.i, src);
       best.slot = __shfl_sync(FULL, best.slot, src);
       best.id = NIL;
-      T3(t_insert);
       return best;
     }
     if (mine) best.id = d_id(C, i1);  // ids only matter for exact ties
     best_reduce(best);
-    T3(t_insert);
     return best;
   }
 #ifdef MC_PHASE_TIMERS3
@@ -898,7 +894,13 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
   const uint32_t lane = lane_id();
   const uint32_t cnt = C.count;
   Bounds b;
+#ifdef MC_PHASE_TIMERS3
+  long long _e3 = clock64();
+#endif
   const Best best = select_victim(C, cnt, b);
+#ifdef MC_PHASE_TIMERS3
+  { long long _n = clock64(); C.t_walk += (unsigned long long)(_n - _e3); _e3 = _n; }
+#endif
   C.c_scan += cnt;
   C.n_evict++;
   if (best.i == NIL) {
@@ -978,6 +980,9 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     C.w.freel()[C.nfree++] = x;
   }
   sync_state(C);
+#ifdef MC_PHASE_TIMERS3
+  C.t_insert += (unsigned long long)(clock64() - _e3);
+#endif
 }
 
 // Split node y at absolute depth x: new upper node [ds, x) takes a new id, y keeps
@@ -1059,7 +1064,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
-  uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL, my_ds = 0, my_de = 0, my_fl = 0;
+  uint32_t v = 0, pos = 0, npath = 0, m = 0, my_path = NIL, my_ds = 0, my_de = 0, my_fl = 0, my_dp = NIL;
   uint32_t partial = NIL, hit = NIL, reuse = 0, hit_idx = NIL;
   uint32_t lin_node = NIL;   // node whose edge strictly contains L_in (when m >= L_in)
   uint32_t lin_bnd = NIL;    // fully matched node ending exactly at L_in
@@ -1079,7 +1084,10 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     const uint32_t cmp = min(len, n - pos);
     const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, off + pos, cmp);
     if (lane == 0 && npath >= 32) C.w.path()[npath] = c;
-    if (lane == npath) { my_path = c; my_ds = pos; my_de = de; my_fl = fl; }
+    if (lane == npath) {
+      my_path = c; my_ds = pos; my_de = de; my_fl = fl;
+      my_dp = C.w.rec()[c].dpos;  // for the pin step; the load overlaps the rest of the walk
+    }
     npath++;
     pinned_bytes += node_bytes(C.m, pos, de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
@@ -1120,9 +1128,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
 
   // Pin the path (R12) and touch only the hit node (step 5): every path
   // lane reads its node's dense position and updates its dense word in parallel.
-  uint32_t my_dp = NIL, old_t = 0;
+  uint32_t old_t = 0;
   if (lane < min(npath, 32u)) {
-    my_dp = C.w.rec()[my_path].dpos;
     DenseRec* d = d_ptr(C, my_dp);
     const uint32_t tc = d->tc;
     if (lane == hit_idx) old_t = tc & T_MASK;
@@ -1220,14 +1227,23 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     // Step 8: insert.
     if (lane == 0 && !C.failed) {
       uint32_t attach = v;  // node at depth m after the splits
-      if (p_split != NIL) {
-        const uint32_t u = split_1(C, P, p_split, p, true, r);
-        if (p == m) attach = u;
+      // splits in depth order: p_split at p (stateful), partial at m (stateless), partial
+      // at n (stateful); one loop keeps a single inlined copy of split_1 (code size)
+      unsigned todo = (p_split != NIL ? 1u : 0u) | (split_m ? 2u : 0u) | (split_n ? 4u : 0u);
+      while (todo) {
+        const int k = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t x = k == 0 ? p : (k == 1 ? m : n);
+        const uint32_t u = split_1(C, P, k == 0 ? p_split : partial, x, k != 1, r);
+        if (k < 2 && x == m) attach = u;
+        if (C.failed) break;
       }
-      if (split_m && !C.failed) attach = split_1(C, P, partial, m, false, r);
-      if (split_n && !C.failed) split_1(C, P, partial, n, true, r);
-      if (p_gain != NIL) gain_1(C, p_gain, r);
-      if (n_gain != NIL) gain_1(C, n_gain, r);
+      unsigned gains = (p_gain != NIL ? 1u : 0u) | (n_gain != NIL ? 2u : 0u);
+      while (gains) {
+        const uint32_t g = (gains & 1u) ? p_gain : n_gain;
+        gains &= gains - 1;
+        gain_1(C, g, r);
+      }
       if (leaf && !C.failed) {
         const uint32_t w = alloc_1(C, P.status);
         if (w != NIL) {
@@ -1304,7 +1320,7 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.moved_slot = NIL;
   C.moved_pos = 0;
   C.bc_valid = 0;
-  C.bc_tmin = 0; C.bc_tmax = 0; C.bc_lo = 0.0f; C.bc_hi = 0.0f;
+  C.bc_tmin = 0; C.bc_tmax = 0; C.bc_lo = 0.0f; C.bc_hi = 0.0f; C.bc_elo = 0.0; C.bc_ehi = 0.0;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
   C.t_walk = C.t_evict = C.t_insert = C.t_unpin = 0;
 #endif

@@ -19,14 +19,14 @@ for it in range(6):
     out["hit_sum"].zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    g.run(out=out)
+    g.run(out=out, **({'n_workers': int(os.environ['NW'])} if os.environ.get('NW') else {}))
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 g.ctx.check()
 cyc = out["cycles"].cpu().numpy().astype(np.float64) * 1024
 ctr = out["counters"].cpu().numpy()
-print(f"{os.path.basename(os.environ.get('MARCONI_LIB', 'default'))} cfg{cfg}: replay ms {np.median(ts[1:]):.2f} "
+print(f"{os.path.basename(os.environ.get('MARCONI_LIB', 'default'))} NW={os.environ.get('NW', '-')} cfg{cfg}: replay ms {np.median(ts[1:]):.2f} "
       f"(min {min(ts[1:]):.2f}) chains {len(g.chains)} chain-cycles median {np.median(cyc)/1e6:.2f}M max {cyc.max()/1e6:.2f}M "
       f"hitsum {int(out['hit_sum'].sum())}", flush=True)
 if os.environ.get("PHASES"):
@@ -34,10 +34,10 @@ if os.environ.get("PHASES"):
     print("phase cycles share walk/evict/insert/unpin:", np.round(tot / tot.sum(), 3), "per request (M):",
           np.round(tot / (len(g.chains) * w.window) / 1e3, 1), "k-cycles")
 if os.environ.get("PHASES3"):
-    tot = ctr.astype(np.float64).sum(0)
+    c = ctr.astype(np.uint64)
     nreq = len(g.chains) * w.window
-    print("per request k-cycles: pass1 %.1f pass2 %.1f verify %.1f ; fallbacks per request %.4f" %
-          (tot[0] / nreq / 1e3, tot[1] / nreq / 1e3, tot[2] / nreq / 1e3, tot[3] / nreq))
-if os.environ.get("PHASES3"):
-    tot_pass1 = (ctr[:, 2].astype(np.uint64) >> np.uint64(32)).sum()
-    print("full bound passes (pass 1) per request: %.3f" % (float(tot_pass1) / (len(g.chains) * w.window)))
+    sel, p2, rem = (c[:, k].astype(np.float64).sum() / nreq / 1e3 for k in range(3))
+    p1 = float((c[:, 3] >> np.uint64(32)).sum()) / nreq
+    fb = float((c[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
+    print("per request k-cycles: select %.1f (pass2 %.1f) removal %.1f ; pass-1 runs/request %.3f fallbacks/request %.4f"
+          % (sel, p2, rem, p1, fb))
