@@ -322,19 +322,25 @@ __device__ __forceinline__ uint32_t hhome(const Chain& C, const HEnt& e) {
   return hslot((e.key >> 14) & SLOT14, e.tok, C.hmask);
 }
 
-// Warp-cooperative lookup of child(parent, tok): 32 probe positions per step, keys
-// compared in registers.  Returns the entry (key == 0 when absent).
+// Warp-cooperative lookup of child(parent, tok).  Linear probing from the home
+// position h, one 128 B line (8 entries) per step: the first step covers h .. end of
+// h's line, later steps whole lines, so a typical lookup (hit or miss at h) touches
+// one or two 32 B sectors instead of a 512 B window.  Returns the entry (key == 0
+// when absent).  hcap is a multiple of 8, so a line never wraps.
 __device__ __forceinline__ HEnt hash_find_warp(const Chain& C, uint32_t parent, uint32_t tok) {
-  const uint32_t h = hslot(parent, tok, C.hmask);
   const uint32_t lane = lane_id();
   const HEnt* __restrict__ tab = C.w.tab();
   HEnt none;
   none.tok = 0; none.key = 0; none.de = 0; none.roff = 0;
-  for (uint32_t base = 0; base <= C.hmask; base += 32) {
-    const HEnt e = tab[(h + base + lane) & C.hmask];
-    const bool valid = hvalid(C, e.key);
+  uint32_t i0 = hslot(parent, tok, C.hmask);
+  for (uint32_t seen = 0; seen <= C.hmask;) {
+    const uint32_t lim = (i0 | 7u) - i0 + 1;  // entries from i0 to the end of its line
+    const bool act = lane < lim;
+    HEnt e = none;
+    if (act) e = tab[i0 + lane];
+    const bool valid = act && hvalid(C, e.key);
     const unsigned mm = __ballot_sync(FULL, valid && hmatch(e, parent, tok));
-    const unsigned me = __ballot_sync(FULL, !valid);
+    const unsigned me = __ballot_sync(FULL, act && !valid);
     if (mm) {
       const int fm = __ffs(mm) - 1;
       HEnt r;
@@ -346,6 +352,8 @@ __device__ __forceinline__ HEnt hash_find_warp(const Chain& C, uint32_t parent, 
       return none;
     }
     if (me) return none;
+    seen += lim;
+    i0 = (i0 + lim) & C.hmask;
   }
   return none;
 }

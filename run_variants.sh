@@ -6,6 +6,6 @@ tail -3 gpurun_out/pytest_gpu.log
 fi
 for i in 1 2; do
 for f in build/variants/*.so; do
-  case $f in *t1*) E="PHASES=1";; *t3*) E="PHASES3=1";; *) E="";; esac
+  case $f in *t1*) E="PHASES=1";; *t3*) E="PHASES3=1";; *t4*) E="PHASES4=1";; *) E="";; esac
   env $E MARCONI_LIB=$PWD/$f timeout 300 python tools/variant_timing.py 2>&1 | tail -2
 done; done | tee gpurun_out/variants.txt

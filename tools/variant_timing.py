@@ -41,3 +41,10 @@ if os.environ.get("PHASES3"):
     fb = float((c[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
     print("per request k-cycles: select %.1f (pass2 %.1f) removal %.1f ; pass-1 runs/request %.3f fallbacks/request %.4f"
           % (sel, p2, rem, p1, fb))
+if os.environ.get("CTR"):
+    nreq = len(g.chains) * w.window
+    print("per request: compared %.1f visited %.2f scanned %.1f written %.2f" % tuple(ctr.astype(np.float64).sum(0) / nreq))
+if os.environ.get("PHASES4"):
+    t = ctr.astype(np.float64).sum(0)
+    print("pass-2 scans: %.0f, entries/scan %.1f, cycles/scan %.0f, cycles per entry-per-lane %.1f"
+          % (t[2], t[1] / t[2], t[0] / t[2], t[0] / (t[1] / 32)))
