@@ -54,6 +54,7 @@ def lib():
         L.orc_destroy.argtypes = [P]
         L.orc_set_alpha.argtypes = [P, D]
         L.orc_set_chunk.argtypes = [P, U32]
+        L.orc_set_block.argtypes = [P, U32]
         L.orc_load.argtypes = [P, P, U32, U32]
         L.orc_step.argtypes = [P, U32, P, P, P]
         L.orc_run.argtypes = [P, U32, U32, P, P, P]
@@ -65,7 +66,7 @@ def lib():
         L.orc_layer_terms.argtypes = [P, U64, P]
         L.orc_node_cost.argtypes = [P, U64, U64, U32, P, P, P]
         L.orc_score_argmin.argtypes = [U32, P, P, P, P, D, P, P]
-        L.orc_run_chains.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, U32, P, U64, P, P, P, U32, P,
+        L.orc_run_chains.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, P, U32, P, U64, P, P, P, U32, P,
                                      P, P, P, P, P, U32]
         _LIB = L
     return _LIB
@@ -138,7 +139,7 @@ class Oracle:
     """One cache (one chain): a radix tree replaying requests of `trace` in order."""
 
     def __init__(self, trace, model, capacity_bytes: int, capacity_nodes: int = 0, alpha: float = 0.0,
-                 chunk: int = 0):
+                 chunk: int = 0, block: int = 0):
         self.h = None
         self.trace = trace
         self._keep = (np.ascontiguousarray(trace.tokens, np.uint32), np.ascontiguousarray(trace.off, np.uint64),
@@ -152,6 +153,8 @@ class Oracle:
         self.h = h
         if chunk:
             _check(lib().orc_set_chunk(self.h, int(chunk)))
+        if block:  # vLLM+ baseline (NEXT-2): token blocks of `block`, LRU
+            _check(lib().orc_set_block(self.h, int(block)))
 
     def close(self):
         if self.h:
@@ -214,6 +217,10 @@ def _chunk(variant) -> int:
     return int(getattr(variant, "chunk_size", 0) or 0)
 
 
+def _block(variant) -> int:
+    return int(getattr(variant, "block_size", 0) or 0)
+
+
 def live_pass(trace, variant, window: int, upto: Optional[int] = None):
     """The α = 0 live LRU pass from an empty cache (SURVEY.md §8(c) c.2 "Segment mode").
 
@@ -222,7 +229,7 @@ def live_pass(trace, variant, window: int, upto: Optional[int] = None):
     after that many requests (default: the whole trace).
     """
     R = trace.n_requests if upto is None else upto
-    o = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, 0.0, _chunk(variant))
+    o = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, 0.0, _chunk(variant), _block(variant))
     snaps = [(np.zeros(0, NODE_DTYPE), 1)]
     hs, fs, bs = [], [], []
     r = 1
@@ -251,6 +258,7 @@ def run_chains(trace, variants: Sequence, chains: Sequence[Tuple[int, float, int
     capb = np.asarray([v.capacity_bytes for v in variants], np.uint64)
     capn = np.asarray([v.capacity_nodes for v in variants], np.uint32)
     chk = np.asarray([_chunk(v) for v in variants], np.uint32)
+    blk = np.asarray([_block(v) for v in variants], np.uint32)
     var = np.asarray([c[0] for c in chains], np.uint32)
     alp = np.asarray([c[1] for c in chains], np.float64)
     first = np.asarray([c[2] for c in chains], np.uint32)
@@ -273,7 +281,7 @@ def run_chains(trace, variants: Sequence, chains: Sequence[Tuple[int, float, int
     o = np.ascontiguousarray(trace.off, np.uint64)
     li = np.ascontiguousarray(trace.lin, np.uint32)
     lo = np.ascontiguousarray(trace.lout, np.uint32)
-    _check(lib().orc_run_chains(models, _ptr(capb), _ptr(capn), _ptr(chk), _ptr(var), _ptr(alp), _ptr(first), _ptr(nreq),
+    _check(lib().orc_run_chains(models, _ptr(capb), _ptr(capn), _ptr(chk), _ptr(blk), _ptr(var), _ptr(alp), _ptr(first), _ptr(nreq),
                                 _ptr(sidx), _ptr(snodes), _ptr(soff), _ptr(snid), nc, _ptr(t), t.shape[0],
                                 _ptr(o), _ptr(li), _ptr(lo), o.shape[0], _ptr(out_off), _ptr(hit),
                                 _ptr(flops), _ptr(byp), _ptr(hsum), _ptr(ctr), n_threads))
@@ -296,7 +304,7 @@ def live_tune(trace, variant, alphas: Sequence[float], multiplier: int = 10, n_t
     bootstrap window (r_F, r_F + multiplier*r_F]; grid replay of that window from the
     snapshot; adopt α* for the rest.  Returns (hits, flops, info)."""
     R = trace.n_requests
-    o = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, 0.0, _chunk(variant))
+    o = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, 0.0, _chunk(variant), _block(variant))
     hits = np.zeros(R, np.uint32)
     flops = np.zeros(R, np.uint64)
     r_f = 0

@@ -125,6 +125,8 @@ struct Node {
   u32 id = 0;
   Node* parent = nullptr;
   std::map<u32, Node*> children;  // keyed by first token of the child's edge
+  // vLLM+ mode (block trie): children keyed by the child's full block content
+  std::map<std::vector<u32>, Node*> bkids;
   std::vector<u32> edge;
   bool has_ssm = false;
   u32 t_last = 0;
@@ -142,10 +144,15 @@ static void collect(Node* n, std::vector<Node*>& out) {  // all non-root nodes, 
     out.push_back(kv.second);
     collect(kv.second, out);
   }
+  for (auto& kv : n->bkids) {
+    out.push_back(kv.second);
+    collect(kv.second, out);
+  }
 }
 
 static void free_subtree(Node* n) {
   for (auto& kv : n->children) free_subtree(kv.second);
+  for (auto& kv : n->bkids) free_subtree(kv.second);
   delete n;
 }
 
@@ -168,8 +175,11 @@ struct Oracle {
   std::vector<orc_evict> log;
   u64 ctr_compared = 0, ctr_visited = 0, ctr_scanned = 0, ctr_written = 0;
 
+  u32 block = 0;  // 0 = Marconi; x > 0 = vLLM+ baseline with token blocks of x (NEXT-2)
+
   ~Oracle() {
     for (auto& kv : root.children) free_subtree(kv.second);
+    for (auto& kv : root.bkids) free_subtree(kv.second);
   }
 
   std::vector<u32> seq(u32 r) const {  // full sequence of request r (1-based)
@@ -197,6 +207,7 @@ struct Oracle {
   // ---- One request: SURVEY.md §8(c) c.2 steps 1-9 ----
   void step(u32 r, u32* hit_out, u64* flops_out, u32* bypass_out) {
     if (r < 1 || r > n_req) fail("request index out of range");
+    if (block) return vstep(r, hit_out, flops_out, bypass_out);
     const std::vector<u32> S = seq(r);
     const u64 n = S.size();
     const u64 L_in = lin[r - 1];
@@ -454,6 +465,106 @@ struct Oracle {
     log.push_back(rec);
   }
 
+  // ---- vLLM+ baseline (readings V1-V8) ----
+  // "fine-grained checkpointing and caches a state for every token block" with
+  // block size x = 32; each block holds the KVs of its x tokens and the
+  // SSM states that represent all prior tokens, vLLM's caching policy
+  // (LRU) extended to hybrid models.  Step by step:
+  //   1. walk the block trie from the root, block k = S[kx, (k+1)x) matched by its
+  //      whole content; only full blocks exist [V1, V2];
+  //   2. hit = the deepest matched block end <= L_in (every block carries a state;
+  //      all-or-nothing) [V4];
+  //   3. every matched block is touched (t_last = r) [V5];
+  //   4. admission of the missing full blocks; bypass when the matched path plus the
+  //      new blocks exceed the capacity [V7];
+  //   5. evict LRU leaf blocks (min (t_last, id)) not on the matched path until the
+  //      new blocks fit [V6];
+  //   6. insert the new blocks, t_last = r.
+  // A block charges node_bytes(x, state) = x tokens of KVs + one set of SSM/conv
+  // states (Appendix A) [V3].
+  void vstep(u32 r, u32* hit_out, u64* flops_out, u32* bypass_out) {
+    const std::vector<u32> S = seq(r);
+    const u64 n = S.size();
+    const u64 L_in = lin[r - 1];
+    if (L_in == 0) fail("input_len == 0 [c.3 #21]");
+    const u64 x = block;
+    const u64 nb = n / x;  // full blocks of the sequence [V2]
+    // Step 1: walk, block content compared token by token.
+    std::vector<Node*> path;
+    Node* v = &root;
+    for (u64 k = 0; k < nb; k++) {
+      std::vector<u32> blk(S.begin() + k * x, S.begin() + (k + 1) * x);
+      auto it = v->bkids.find(blk);
+      if (it == v->bkids.end()) break;
+      v = it->second;
+      path.push_back(v);
+    }
+    const u64 mb = path.size();
+    ctr_compared += mb * x;
+    ctr_visited += mb + 1;
+    // Step 2: hit [V4].
+    const u64 reuse = std::min<u64>(mb, L_in / x) * x;
+    // Step 3: touch the matched path [V5].
+    for (Node* c : path) c->t_last = r;
+    ctr_written += mb;
+    // Step 4: admission [V7].
+    const u64 bb = node_bytes(x, true, model);
+    const u64 n_new = nb - mb;
+    const u64 d_bytes = bb * n_new;
+    const u64 pinned_bytes = bb * mb;
+    const bool bypass = (pinned_bytes + d_bytes > cap_bytes) || (cap_nodes && mb + n_new > cap_nodes);
+    if (!bypass) {
+      // Step 5: LRU leaf eviction [V6].
+      while (total_incremental + d_bytes > cap_bytes || (cap_nodes && count_nodes() + n_new > cap_nodes))
+        vevict_one(r, path);
+      // Step 6: insert the missing blocks under the deepest matched one.
+      for (u64 k = mb; k < nb; k++) {
+        Node* c = new Node();
+        c->id = next_id++;
+        c->parent = v;
+        c->edge.assign(S.begin() + k * x, S.begin() + (k + 1) * x);
+        c->has_ssm = true;
+        c->t_last = r;
+        c->ref_off = off[r - 1];
+        v->bkids[c->edge] = c;
+        v = c;
+        ctr_written += 1;
+      }
+      total_incremental += d_bytes;
+      if (total_bytes() != total_incremental) fail("byte accounting mismatch");
+      if (total_incremental > cap_bytes) fail("capacity exceeded");
+      if (cap_nodes && count_nodes() > cap_nodes) fail("node capacity exceeded");
+    }
+    if (reuse > L_in) fail("hit exceeds input length");
+    *hit_out = (u32)reuse;
+    *flops_out = prefill_flops(reuse, model);
+    *bypass_out = bypass ? 1u : 0u;
+  }
+
+  // One LRU eviction among the leaf blocks off the pinned path [V6]; the logged
+  // utility is Eq. 2 at alpha = 0 (the recency term) for the log format.
+  void vevict_one(u32 r, const std::vector<Node*>& pinned) {
+    std::vector<Node*> all;
+    collect(&root, all);
+    if (all.empty()) fail("nothing to evict");
+    ctr_scanned += all.size();
+    u32 tmin = all[0]->t_last, tmax = all[0]->t_last;
+    for (Node* x : all) { tmin = std::min(tmin, x->t_last); tmax = std::max(tmax, x->t_last); }
+    Node* best = nullptr;
+    for (Node* x : all) {
+      if (!x->bkids.empty()) continue;  // only leaf blocks: an inner block's descendants need it
+      if (std::find(pinned.begin(), pinned.end(), x) != pinned.end()) continue;
+      if (!best || x->t_last < best->t_last || (x->t_last == best->t_last && x->id < best->id)) best = x;
+    }
+    if (!best) fail("no eviction candidate");
+    const double u = (tmax == tmin) ? 0.5 : (double)(best->t_last - tmin) / (double)(tmax - tmin);
+    log.push_back(orc_evict{r, best->id, 0, (u32)all.size(), u});
+    total_incremental -= node_bytes(best->edge.size(), best->has_ssm, model);
+    best->parent->bkids.erase(best->edge);
+    delete best;
+    ctr_written += 1;
+  }
+
   // ---- snapshots (canonical dump) ----
   std::vector<orc_node> dump() {
     std::vector<Node*> all;
@@ -477,7 +588,9 @@ struct Oracle {
 
   void load(const orc_node* nodes, u32 n, u32 nid) {
     for (auto& kv : root.children) free_subtree(kv.second);
+    for (auto& kv : root.bkids) free_subtree(kv.second);
     root.children.clear();
+    root.bkids.clear();
     std::map<u32, Node*> by_id;
     by_id[0] = &root;
     for (u32 i = 0; i < n; i++) {
@@ -497,6 +610,12 @@ struct Oracle {
       if (it == by_id.end()) fail("snapshot parent missing");
       Node* x = by_id[nodes[i].id];
       x->parent = it->second;
+      if (block) {
+        if (x->edge.size() != block || nodes[i].d_start % block) fail("snapshot record is not one block");
+        if (it->second->bkids.count(x->edge)) fail("snapshot block trie property violated");
+        it->second->bkids[x->edge] = x;
+        continue;
+      }
       if (it->second->children.count(x->edge[0])) fail("snapshot radix property violated");
       it->second->children[x->edge[0]] = x;
     }
@@ -601,6 +720,8 @@ void* orc_create(const orc_model* m, u64 cap_bytes, u32 cap_nodes, double alpha,
 }
 void orc_destroy(void* h) { delete (Oracle*)h; }
 int orc_set_chunk(void* h, u32 chunk) { ORC_TRY(((Oracle*)h)->chunk = chunk) }
+// vLLM+ baseline with token blocks of `block` (0 = Marconi); set before any step/load.
+int orc_set_block(void* h, u32 block) { ORC_TRY(((Oracle*)h)->block = block) }
 int orc_set_alpha(void* h, double a) {
   ORC_TRY(if (!(a >= 0)) throw std::invalid_argument("alpha < 0"); ((Oracle*)h)->alpha = a)
 }
@@ -645,6 +766,7 @@ int orc_total(void* h, u64* total, u64* count) {
 // snap_nodes[snap_off[s] .. snap_off[s+1]) with s = snap_idx[c]; outputs are
 // written at hit[out_off[c] + i].  hit_sum[c] = sum of hits.
 int orc_run_chains(const orc_model* models, const u64* cap_bytes, const u32* cap_nodes, const u32* chunks,
+                   const u32* blocks,
                    const u32* variant, const double* alpha, const u32* first, const u32* n,
                    const u32* snap_idx, const orc_node* snap_nodes, const u64* snap_off,
                    const u32* snap_next_id, u32 n_chains, const u32* tokens, u64 n_tokens,
@@ -666,6 +788,7 @@ int orc_run_chains(const orc_model* models, const u64* cap_bytes, const u32* cap
                                           n_tokens, off, lin, lout, n_req);
           if (!o) throw std::runtime_error(g_err);
           o->chunk = chunks ? chunks[v] : 0;
+          o->block = blocks ? blocks[v] : 0;
           u32 s = snap_idx[c];
           o->load(snap_nodes + snap_off[s], (u32)(snap_off[s + 1] - snap_off[s]), snap_next_id[s]);
           u64 sum = 0;

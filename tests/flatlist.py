@@ -287,3 +287,87 @@ def opt_reuse(trace, model, cap_bytes, cap_nodes) -> int:
 
     rec(FlatCache(model, cap_bytes, cap_nodes, 0.0), 1, 0, [])
     return best[0]
+
+
+# ----------------------------------------------------------------------------
+# vLLM+ baseline (readings V1-V8), brute force.
+# ----------------------------------------------------------------------------
+class FlatBlocks:
+    """Block-granular cache as an unordered list of entries (path = the full token
+    prefix S[:jx] a block ends, t_last, id); relations by brute force on each query:
+
+      parent(e)  = the entry whose path is e.path minus its last x tokens (or root)
+      leaf(e)    = no entry has e as parent
+      matched mb = largest k with S[:jx] cached for every j <= k
+      block bytes = x tokens of KVs + one set of SSM/conv states
+
+    Lookup hit = min(mb, L_in // x) * x (every block carries a state, PAPER:300);
+    every matched block and every inserted one gets t_last = r; LRU over leaf blocks
+    off the matched path, min (t_last, id) ("vLLM's caching policy").
+    Shares nothing with oracle/oracle.cpp (no trie, no maps keyed by content)."""
+
+    def __init__(self, model, cap_bytes: int, cap_nodes: int, x: int):
+        self.m, self.cap_bytes, self.cap_nodes, self.x = model, cap_bytes, cap_nodes, x
+        self.E: Dict[int, Entry] = {}
+        self.next_id = 1
+        self.log: List[Tuple[int, int, int, float]] = []
+
+    def bb(self) -> int:
+        return KVT(self.m) * self.x + SSMB(self.m)
+
+    def cached(self, p) -> Optional[Entry]:
+        for e in self.E.values():
+            if e.path == tuple(p):
+                return e
+        return None
+
+    def is_leaf(self, e: Entry) -> bool:
+        return not any(len(f.path) == len(e.path) + self.x and f.path[:len(e.path)] == e.path
+                       for f in self.E.values())
+
+    def step(self, r: int, inp, out):
+        S = tuple(inp) + tuple(out)
+        n, L_in, x = len(S), len(inp), self.x
+        nb = n // x
+        mb = 0
+        while mb < nb and self.cached(S[:(mb + 1) * x]) is not None:
+            mb += 1
+        reuse = min(mb, L_in // x) * x
+        path = [self.cached(S[:(j + 1) * x]) for j in range(mb)]
+        for e in path:
+            e.t = r
+        bb = self.bb()
+        n_new = nb - mb
+        bypass = (mb + n_new) * bb > self.cap_bytes or bool(self.cap_nodes and nb > self.cap_nodes)
+        if not bypass:
+            pids = {id(e) for e in path}
+            while (len(self.E) + n_new) * bb > self.cap_bytes or (self.cap_nodes and len(self.E) + n_new > self.cap_nodes):
+                ts = [e.t for e in self.E.values()]
+                tmin, tmax = min(ts), max(ts)
+                cands = [e for e in self.E.values() if id(e) not in pids and self.is_leaf(e)]
+                assert cands, "no candidate"
+                v = min(cands, key=lambda e: (e.t, e.id))
+                u = 0.5 if tmax == tmin else float(v.t - tmin) / float(tmax - tmin)
+                self.log.append((r, v.id, 0, u))
+                del self.E[v.id]
+            for j in range(mb, nb):
+                self.E[self.next_id] = Entry(S[:(j + 1) * x], True, r, self.next_id)
+                self.next_id += 1
+        return reuse, F(reuse, self.m), int(bool(bypass))
+
+    def dump(self):
+        out = []
+        for e in sorted(self.E.values(), key=lambda e: e.id):
+            par = self.cached(e.path[:-self.x]) if len(e.path) > self.x else None
+            out.append((e.id, par.id if par else 0, len(e.path) - self.x, len(e.path), 1, e.t))
+        return out
+
+
+def replay_blocks(trace, model, cap_bytes, cap_nodes, x):
+    c = FlatBlocks(model, cap_bytes, cap_nodes, x)
+    res = []
+    for r in range(1, trace.n_requests + 1):
+        s = trace.seq(r)
+        L = int(trace.lin[r - 1])
+        res.append(c.step(r, [int(t) for t in s[:L]], [int(t) for t in s[L:]]))
+    return res, c

@@ -127,6 +127,7 @@ class Variant:
     capacity_bytes: int
     capacity_nodes: int = 0
     chunk_size: int = 0  # 0 = exact checkpoints; else chunk-aligned prefill checkpoints (NEXT-3)
+    block_size: int = 0  # 0 = Marconi; x > 0 = the vLLM+ baseline with token blocks of x (NEXT-2)
 
 
 @dataclasses.dataclass
