@@ -71,12 +71,23 @@ typedef struct {
  * chunk_size = 0: exact checkpoint positions (two-pass prefill);
  * chunk_size = c > 0: chunked state passing -- the prefill (branch) checkpoint is
  * placed at the multiple of c at or below the branch point and skipped if that is 0
- * or not beyond the hit; decode checkpoints stay exact. */
+ * or not beyond the hit; decode checkpoints stay exact.
+ * block_size = 0: the Marconi policy above.  block_size = x > 0: the vLLM+
+ * baseline instead: "fine-grained checkpointing ... a state
+ * for every token block" of x tokens (PAPER:302, PAPER:532 uses x = 32) with vLLM's
+ * LRU policy -- every full block of a sequence is a cache node holding its KVs and
+ * the SSM states at its end; a hit is the deepest cached block boundary <= the
+ * input length; the matched blocks are touched; LRU evicts leaf blocks (min
+ * (t_last, id)); the readings are DESIGN.md V1-V8.  α is ignored (chains of a
+ * vLLM+ variant replay identically for every α).  chunk_size must be 0 then.
+ * reserved must be 0. */
 typedef struct {
   mc_model model;
   uint64_t capacity_bytes;
   uint32_t capacity_nodes;
   uint32_t chunk_size;
+  uint32_t block_size;
+  uint32_t reserved;
 } mc_variant;
 
 /* Request r (1-based, at index r-1): sequence = tokens[tok_off, tok_off + input_len
@@ -88,7 +99,9 @@ typedef struct {
 
 /* Canonical snapshot record (one radix node).  id 0 is the root (never listed);
  * parent_id 0 = child of the root.  The node's edge is tokens[ref_off + d_start,
- * ref_off + d_end); its SSM state (if has_ssm) represents depth d_end. */
+ * ref_off + d_end); its SSM state (if has_ssm) represents depth d_end.  For a
+ * vLLM+ variant every record is one block: d_end - d_start = block_size,
+ * d_start a multiple of it, has_ssm = 1. */
 typedef struct {
   uint32_t id, parent_id;
   uint64_t ref_off;

@@ -48,6 +48,9 @@ constexpr int kWarpsPerCta = MC_WARPS_PER_CTA;
 // ---------------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------------
+// kPolicy 0 = Marconi chains, 1 = vLLM+ chains (block_size > 0): one instantiation per
+// policy so the Marconi kernel carries no vLLM+ code (registers, instruction cache).
+template <int kPolicy>
 __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel(KParams P) {
   extern __shared__ __align__(16) char smem[];
   const uint32_t lane = lane_id();
@@ -76,7 +79,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     Prefetched cur = fetch_request(P, seg.first_req), nxt = cur;
     for (uint32_t i = 0; i < seg.n_req && !C.failed; i++) {
       const uint32_t r = seg.first_req + i;
-      const ReqOut o = process_request(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n);
+      const ReqOut o = kPolicy ? process_request_vllm(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n)
+                               : process_request(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n);
       cur = nxt;
       if (lane == 0) {
         P.hit[obase + r - 1] = o.reuse;
@@ -120,7 +124,8 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   Prefetched cur = fetch_request(P, 1), nxt = cur;
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
     const uint32_t ev0 = C.n_evict;
-    const ReqOut o = process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
+    const ReqOut o = C.block ? process_request_vllm(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr)
+                             : process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
     cur = nxt;
     if (first == 0 && C.n_evict != ev0) first = r;  // the paper's "first eviction"
     if (lane == 0) {
@@ -295,6 +300,10 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
       return fail(MC_EINVAL, "bytes_per_param must be 1, 2 or 4 (SPEC:36)");
     if (m.n_attn == 0) return fail(MC_EINVAL, "n_attn = 0 would allow zero-byte nodes (SPEC:136)");
     if (m.d_model == 0) return fail(MC_EINVAL, "d_model must be >= 1");
+    if (hv[v].block_size && hv[v].chunk_size)
+      return fail(MC_EINVAL, "block_size (vLLM+) and chunk_size (Marconi chunked prefill) are exclusive");
+    if (hv[v].block_size > (1u << 20)) return fail(MC_EINVAL, "block_size must be <= 2^20");
+    if (hv[v].reserved) return fail(MC_EINVAL, "mc_variant.reserved must be 0");
     // F(L) must stay exact in fp64 (< 2^53) for L up to 2^20 tokens handled below per trace
   }
   CU(cudaSetDevice(device));
@@ -319,10 +328,11 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     c->smem_nodes = std::min<uint32_t>(c->smem_nodes, max_nodes);
     c->smem_nodes_live = std::min<uint32_t>((uint32_t)((smem_optin / 8) & ~31), max_nodes);
   }
-  cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(replay_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(replay_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaFuncSetAttribute(live_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel, 32 * kWarpsPerCta,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel<0>, 32 * kWarpsPerCta,
                                                 kWarpsPerCta * 8ull * c->smem_nodes);
   c->blocks_per_sm = std::max(1, bps);
   c->ncap = max_nodes;
@@ -334,6 +344,8 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     d.cap_bytes = hv[v].capacity_bytes;
     d.cap_nodes = hv[v].capacity_nodes;
     d.chunk = hv[v].chunk_size;
+    d.block = hv[v].block_size;
+    d.pad = 0;
     c->dvh.push_back(d);
   }
   c->snaps.resize(n_var);
@@ -622,14 +634,18 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
         return fail(MC_ESTATE, "segment snapshot index missing for variant " + std::to_string(v));
   const uint32_t n_chains = A->h_chains ? A->n_chains : (uint32_t)total_chains;
   if (n_chains == 0) return MC_OK;
+  // chain ids, Marconi chains first, then vLLM+ chains (each group keeps the caller's order)
   std::vector<uint32_t> ids;
-  if (A->h_chains) {
-    for (uint32_t i = 0; i < n_chains; i++)
-      if (A->h_chains[i] >= total_chains) return fail(MC_EINVAL, "chain id out of range");
-  } else {
-    ids.resize(n_chains);
-    for (uint32_t i = 0; i < n_chains; i++) ids[i] = i;
-  }
+  ids.reserve(n_chains);
+  uint32_t n_marconi = 0;
+  for (int pass = 0; pass < 2; pass++)
+    for (uint32_t i = 0; i < n_chains; i++) {
+      const uint32_t id = A->h_chains ? A->h_chains[i] : i;
+      if (id >= total_chains) return fail(MC_EINVAL, "chain id out of range");
+      const bool vl = c->hv[id / (ns * A->n_alpha)].block_size != 0;
+      if (vl == (pass == 1)) ids.push_back(id);
+      if (pass == 0 && !vl) n_marconi++;
+    }
   const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
   if (A->workspace_bytes < head + per) return fail(MC_ENOMEM, "workspace too small");
@@ -639,7 +655,7 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)A->d_workspace;
   CU(cudaMemsetAsync(ws, 0, 256, st));
-  CU(cudaMemcpyAsync(ws + kCtrl, A->h_chains ? A->h_chains : ids.data(), 4ull * n_chains, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(ws + kCtrl, ids.data(), 4ull * n_chains, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(c->d_alphas, A->h_alphas, sizeof(double) * A->n_alpha, cudaMemcpyHostToDevice, st));
   KParams P;
   memset(&P, 0, sizeof(P));
@@ -676,9 +692,24 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   S = std::min<uint32_t>(S, c->ncap) & ~31u;
   if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
   P.smem_nodes = S;
-  const uint32_t ctas = (workers + kWarpsPerCta - 1) / kWarpsPerCta;
-  replay_kernel<<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
-  CU(cudaGetLastError());
+  // one launch per policy group, back to back on `st` (they share the worker slices);
+  // each launch has its own queue word
+  const uint32_t groups[2] = {n_marconi, n_chains - n_marconi};
+  uint32_t first = 0;
+  for (int g = 0; g < 2; g++) {
+    if (groups[g] == 0) continue;
+    P.chains = (const uint32_t*)(ws + kCtrl) + first;
+    P.n_chains = groups[g];
+    P.queue = (unsigned*)ws + 16 * g;
+    P.n_workers = std::min(workers, groups[g]);
+    const uint32_t ctas = (P.n_workers + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (g == 0)
+      replay_kernel<0><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
+    else
+      replay_kernel<1><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
+    CU(cudaGetLastError());
+    first += groups[g];
+  }
   return MC_OK;
 }
 

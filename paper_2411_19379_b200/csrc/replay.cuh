@@ -72,6 +72,7 @@ struct DevVariant {
   DevModel m;
   uint64_t cap_bytes;
   uint32_t cap_nodes, chunk;  // chunk = 0: exact checkpoints; else chunk-aligned prefill checkpoints
+  uint32_t block, pad;        // block > 0: the vLLM+ baseline with token blocks of `block` (NEXT-2)
 };
 struct DevSnapStore {
   const mc_snap_node* nodes;
@@ -256,6 +257,8 @@ struct Chain {
   DevModel m;
   uint64_t capb;
   uint32_t capn, chunk;
+  uint32_t block;  // > 0: vLLM+ baseline (token blocks of `block`), else Marconi
+  uint32_t mthr;   // D_MULTI threshold: children that make a node a non-candidate (2 Marconi, 1 vLLM+)
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
@@ -437,7 +440,7 @@ __device__ __forceinline__ void d_stamp(Chain& C, uint32_t i, uint32_t t) {
 }
 __device__ __forceinline__ void d_multi(Chain& C, uint32_t i, uint32_t nchild) {
   DenseRec* d = d_ptr(C, i);
-  d->tc = (d->tc & ~D_MULTI) | (nchild >= 2 ? D_MULTI : 0u);
+  d->tc = (d->tc & ~D_MULTI) | (nchild >= C.mthr ? D_MULTI : 0u);
 }
 __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   const uint32_t i = C.count++;
@@ -448,7 +451,7 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
   d->e32 = __double2float_rn(v);
-  d->tc = t | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u);
+  d->tc = t | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
   bc_add(C, t, d->e32, v);
 }
 __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
@@ -459,6 +462,31 @@ __device__ __forceinline__ uint32_t alloc_1(Chain& C, uint32_t* status) {
     return NIL;
   }
   return C.hwm++;
+}
+
+// ---- vLLM+ block keys: content hash of a token block (sum of position-mixed tokens,
+// so one lane or a whole warp computes the same value); equal hashes are always
+// verified against the tokens, so collisions cost time, never correctness ----
+__device__ __forceinline__ uint32_t tok_mix(uint32_t t, uint32_t j) {
+  uint32_t h = t ^ (j * 0x9E3779B9u);
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ uint32_t block_hash_1(const uint32_t* __restrict__ p, uint32_t x) {
+  uint32_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+  uint32_t j = 0;
+  for (; j + 4 <= x; j += 4) {
+    h0 += tok_mix(__ldg(p + j), j);
+    h1 += tok_mix(__ldg(p + j + 1), j + 1);
+    h2 += tok_mix(__ldg(p + j + 2), j + 2);
+    h3 += tok_mix(__ldg(p + j + 3), j + 3);
+  }
+  for (; j < x; j++) h0 += tok_mix(__ldg(p + j), j);
+  return (h0 + h1) + (h2 + h3);
 }
 
 // ---------------------------------------------------------------------------
@@ -511,6 +539,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     const uint32_t s = i + 1;
     const uint32_t pi = pidx[i];
     bad |= (r.d_end <= r.d_start) || (r.ref_off + r.d_end > P.n_tok) || (pi != NIL && pi >= n);
+    if (C.block) bad |= (r.d_end - r.d_start != C.block) || (r.d_start % C.block) || !r.has_ssm;
     NodeRec R;
     R.parent = (pi == NIL) ? 0u : pi + 1;
     R.hidx = NIL;
@@ -529,7 +558,9 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec& R = C.w.rec()[s];
-    const uint32_t ps = R.parent, ft = P.tok[(uint64_t)R.roff + R.ds];
+    const uint32_t ps = R.parent;
+    // child-index key token: the edge's first token (Marconi) or the block's content hash (vLLM+)
+    const uint32_t ft = C.block ? block_hash_1(P.tok + R.roff + R.ds, C.block) : P.tok[(uint64_t)R.roff + R.ds];
     atomicAdd(&C.w.rec()[ps].nf, 1u);
     atomicXor(&C.w.rec()[ps].cxor, s);
     uint32_t j = hslot(ps, ft, C.hmask);
@@ -552,7 +583,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
     C.w.eff64()[i] = v;
     DenseRec* d = d_ptr(C, i);
-    d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= 2 ? D_MULTI : 0u);
+    d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
     d->e32 = __double2float_rn(v);
   }
 #pragma unroll
@@ -1308,6 +1339,189 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   return o;
 }
 
+// ---------------------------------------------------------------------------
+// vLLM+ baseline (readings V1-V8): a state per
+// token block, vLLM's LRU policy.  Every full block of a
+// sequence is one node; its child-index key is (parent, content hash) and every
+// hash match is verified against the tokens.  Same workspace, dense list, victim
+// selection (α = 0 LRU pass over leaf blocks) and removal as the Marconi path.
+// ---------------------------------------------------------------------------
+
+// Child of `parent` whose block equals tokens[b0, b0 + x) (hash h), or NIL.  Walks
+// the probe sequence line by line; every (parent, h) match is verified with a token
+// compare (collisions are skipped, so the result is exact).
+__device__ __forceinline__ uint32_t child_block(const Chain& C, const KParams& P, uint32_t parent, uint32_t h,
+                                                uint64_t b0, uint32_t kx) {
+  const uint32_t lane = lane_id();
+  const HEnt* __restrict__ tab = C.w.tab();
+  const uint32_t x = C.block;
+  uint32_t i0 = hslot(parent, h, C.hmask);
+  for (uint32_t seen = 0; seen <= C.hmask;) {
+    const uint32_t lim = (i0 | 7u) - i0 + 1;
+    const bool act = lane < lim;
+    HEnt e;
+    e.tok = 0; e.key = 0; e.de = 0; e.roff = 0;
+    if (act) e = tab[i0 + lane];
+    const bool valid = act && hvalid(C, e.key);
+    const unsigned me = __ballot_sync(FULL, act && !valid);
+    unsigned mm = __ballot_sync(FULL, valid && hmatch(e, parent, h));
+    if (me) mm &= (1u << (__ffs(me) - 1)) - 1u;  // only entries before the first empty slot
+    while (mm) {
+      const int fm = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const uint32_t roff = __shfl_sync(FULL, e.roff, fm);
+      const uint32_t key = __shfl_sync(FULL, e.key, fm);
+      if (match_len(P.tok, (uint64_t)roff + kx, b0, x) == x) return key & SLOT14;
+    }
+    if (me) return NIL;
+    seen += lim;
+    i0 = (i0 + lim) & C.hmask;
+  }
+  return NIL;
+}
+
+__device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, const Prefetched cur,
+                                       Prefetched& nxt, bool has_next, mc_evict_rec* log, uint32_t* log_n) {
+  const uint32_t lane = lane_id();
+  const mc_request q = cur.q;
+  const uint64_t off = q.tok_off;
+  const uint32_t L_in = q.input_len;
+  const uint32_t n = q.input_len + q.output_len;
+  const uint32_t x = C.block;
+  const uint32_t nb = n / x;  // full blocks; a trailing partial block is not cached (V2)
+  if (has_next) nxt.q = P.req[r];
+  uint32_t* __restrict__ path = C.w.path();
+
+  // Step 1: walk block by block (V1).  Block hashes are computed 32 at a time, one
+  // block per lane, ahead of the dependent child-index probes.
+  uint32_t v = 0, mb = 0;
+  if (nb > C.ncap) {  // the sequence's blocks cannot all be held: the path array bounds the walk
+    if (lane == 0) atomicOr(P.status, ST_OVERFLOW);
+    C.failed = true;
+    ReqOut o;
+    o.reuse = 0; o.flops = 0; o.bypass = true;
+    return o;
+  }
+  for (uint32_t k0 = 0; k0 < nb && mb == k0; k0 += 32) {
+    const uint32_t kl = k0 + lane;
+    const uint32_t my_h = (kl < nb) ? block_hash_1(P.tok + off + (uint64_t)kl * x, x) : 0u;
+    const uint32_t kend = min(nb, k0 + 32);
+    for (uint32_t k = k0; k < kend; k++) {
+      const uint32_t h = __shfl_sync(FULL, my_h, k - k0);
+      const uint32_t c = child_block(C, P, v, h, off + (uint64_t)k * x, k * x);
+      if (c == NIL) break;
+      if (lane == 0) path[k] = c;
+      v = c;
+      mb++;
+    }
+  }
+  __syncwarp();
+  C.c_cmp += (uint64_t)mb * x;
+  C.c_vis += mb + 1;
+  if (has_next) nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
+
+  // Step 2: hit = the deepest matched block end <= L_in (V4).
+  const uint32_t reuse = min(mb, L_in / x) * x;
+
+  // Step 3: touch (t_last = r) and pin every matched block (V5, V7), in parallel.
+  for (uint32_t i = lane; i < mb; i += 32) {
+    DenseRec* d = d_ptr(C, C.w.rec()[path[i]].dpos);
+    d->tc = r | (d->tc & D_MULTI) | D_PIN;
+  }
+  C.c_wr += mb;
+  __syncwarp();
+
+  // Step 4: admission (V7): bypass when the matched path plus the new blocks exceed the capacity.
+  const uint64_t bb = node_bytes(C.m, 0, x, true);
+  const uint32_t n_new = nb - mb;
+  const uint64_t d_bytes = bb * n_new;
+  const bool bypass = (bb * mb + d_bytes > C.capb) || (C.capn && nb > C.capn);
+  if (!bypass) {
+    // Step 5: LRU leaf eviction (V6) until the new blocks fit.
+    while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + n_new > C.capn)))
+      evict_one(C, P, r, log, log_n);
+    // Step 6: insert blocks mb .. nb-1 under v, in parallel (one block per lane).
+    if (n_new && !C.failed) {
+      const uint32_t take = min(C.nfree, n_new);
+      if (C.hwm + (n_new - take) > C.ncap) {
+        if (lane == 0) atomicOr(P.status, ST_OVERFLOW);
+        C.failed = true;
+      } else {
+        for (uint32_t j = lane; j < n_new; j += 32)
+          path[mb + j] = (j < take) ? C.w.freel()[C.nfree - 1 - j] : C.hwm + (j - take);
+        __syncwarp();
+        const uint32_t cnt0 = C.count, id0 = C.next_id;
+        for (uint32_t j = lane; j < n_new; j += 32) {
+          const uint32_t k = mb + j;
+          const uint32_t s = path[k];
+          const uint32_t par = (j == 0) ? v : path[k - 1];
+          const bool inner = j + 1 < n_new;
+          NodeRec R;
+          R.parent = par;
+          R.ds = k * x;
+          R.de = (k + 1) * x;
+          R.roff = (uint32_t)off;
+          R.cxor = inner ? path[k + 1] : 0u;
+          R.nf = (F_SSM << 24) | (inner ? 1u : 0u);
+          R.dpos = cnt0 + j;
+          const uint32_t h = block_hash_1(P.tok + off + (uint64_t)k * x, x);
+          uint32_t hi = hslot(par, h, C.hmask);
+          const uint32_t nk = hkey(C, par, s);
+          for (;;) {  // lanes insert concurrently: claim an empty slot by CAS on its key word
+            const uint32_t kw = atomicAdd(&C.w.tab()[hi].key, 0u);
+            if (hvalid(C, kw)) { hi = (hi + 1) & C.hmask; continue; }
+            if (atomicCAS(&C.w.tab()[hi].key, kw, nk) == kw) break;
+          }
+          HEnt& E = C.w.tab()[hi];
+          E.tok = h;
+          E.de = R.de | 0x80000000u;
+          E.roff = R.roff;
+          R.hidx = hi;
+          C.w.rec()[s] = R;
+          C.w.ids()[s] = id0 + j;
+          d_set_slot(C, cnt0 + j, s);
+          C.w.eff64()[cnt0 + j] = 0.0;  // unused by LRU
+          DenseRec* d = d_ptr(C, cnt0 + j);
+          d->tc = r | (inner ? D_MULTI : 0u);
+          d->e32 = 0.0f;
+        }
+        if (lane == 0) {
+          NodeRec& Rv = C.w.rec()[v];
+          const uint32_t nf0 = Rv.nf;
+          Rv.nf = nf0 + 1;
+          Rv.cxor ^= path[mb];
+          if (v != 0 && (nf0 & NCH_MASK) + 1 >= C.mthr) {
+            DenseRec* d = d_ptr(C, Rv.dpos);
+            d->tc |= D_MULTI;
+          }
+          C.nfree -= take;
+          C.hwm += n_new - take;
+          C.count = cnt0 + n_new;
+          C.next_id = id0 + n_new;
+          C.total += d_bytes;
+          C.c_wr += n_new;
+          if (C.total > C.capb || (C.capn && C.count > C.capn)) {
+            atomicOr(P.status, ST_INVARIANT);
+            C.failed = true;
+          }
+        }
+      }
+    }
+    sync_state(C);
+  }
+  // Unpin the matched path (evictions may have moved dense entries: positions re-read).
+  for (uint32_t i = lane; i < mb; i += 32) {
+    DenseRec* d = d_ptr(C, C.w.rec()[path[i]].dpos);
+    d->tc &= ~D_PIN;
+  }
+  __syncwarp();
+  ReqOut o;
+  o.reuse = reuse;
+  o.flops = prefill_F(C.m, reuse);
+  o.bypass = bypass;
+  return o;
+}
+
 __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t worker, const DevVariant& V,
                                            double alpha, char* smem_warp, uint32_t S) {
   C.w.b = P.ws + (uint64_t)worker * P.ws_stride;
@@ -1322,7 +1536,9 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.capb = V.cap_bytes;
   C.capn = V.cap_nodes;
   C.chunk = V.chunk;
-  C.alpha = alpha;
+  C.block = V.block;
+  C.mthr = V.block ? 1u : 2u;  // vLLM+ evicts leaf blocks only (V6)
+  C.alpha = V.block ? 0.0 : alpha;  // vLLM+ is LRU: α does not apply
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;
   C.moved_slot = NIL;

@@ -41,7 +41,7 @@ class mc_model(C.Structure):
 
 class mc_variant(C.Structure):
     _fields_ = [("model", mc_model), ("capacity_bytes", C.c_uint64), ("capacity_nodes", C.c_uint32),
-                ("chunk_size", C.c_uint32)]
+                ("chunk_size", C.c_uint32), ("block_size", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class mc_replay_args(C.Structure):
@@ -119,8 +119,11 @@ def _stream_ptr(stream) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
-def make_variant(model, capacity_bytes: int, capacity_nodes: int = 0, chunk_size: int = 0) -> mc_variant:
-    return mc_variant(mc_model(*model.astuple()), int(capacity_bytes), int(capacity_nodes), int(chunk_size))
+def make_variant(model, capacity_bytes: int, capacity_nodes: int = 0, chunk_size: int = 0,
+                 block_size: int = 0) -> mc_variant:
+    """block_size > 0 selects the vLLM+ baseline (token blocks of that size, NEXT-2)."""
+    return mc_variant(mc_model(*model.astuple()), int(capacity_bytes), int(capacity_nodes), int(chunk_size),
+                      int(block_size), 0)
 
 
 def requests_array(off, lin, lout) -> np.ndarray:
@@ -147,7 +150,8 @@ class Context:
         self.device = torch.device("cuda", device)
         self.variants = list(variants)
         arr = (mc_variant * len(self.variants))(*[make_variant(v.model, v.capacity_bytes, v.capacity_nodes,
-                                                                getattr(v, "chunk_size", 0))
+                                                                getattr(v, "chunk_size", 0),
+                                                                getattr(v, "block_size", 0))
                                                    for v in self.variants])
         h = C.c_void_p()
         check(lib().mc_create(arr, len(self.variants), int(max_nodes), int(device), C.byref(h)))

@@ -53,7 +53,8 @@ def oracle_grid(trace, variants, alphas, n_segments, threads=0, chains=None):
 
 
 def oracle_chain_log(trace, var, alpha, first, n, snap):
-    o = O.Oracle(trace, var.model, var.capacity_bytes, var.capacity_nodes, alpha, getattr(var, "chunk_size", 0))
+    o = O.Oracle(trace, var.model, var.capacity_bytes, var.capacity_nodes, alpha, getattr(var, "chunk_size", 0),
+                 getattr(var, "block_size", 0))
     o.load(*snap)
     h, f, b = o.run(first, n)
     lg = o.log()

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_sizes_match_header():
     assert ctypes.sizeof(M.mc_model) == 32
-    assert ctypes.sizeof(M.mc_variant) == 48
+    assert ctypes.sizeof(M.mc_variant) == 56
     assert M.REQUEST_DTYPE.itemsize == 16
     assert M.SNAP_DTYPE.itemsize == 32
     assert ctypes.sizeof(M.mc_replay_args) == 128  # 11 pointers/u64 + 6 u32 (+pad), see include/marconi.h

@@ -444,3 +444,92 @@ def test_arrival_sweep(rate, delay):
     """fig:micro_arrival axes: session rate 0.5 -> 2 /s, response time 5 -> 10 s."""
     w = tg.arrival_workload(rate, delay, R=6000, n_segments=12, alphas=(0.0, 0.25, 4.0))
     _compare_grid(w)
+
+
+# ---------------------------------------------------------------- NEXT-2: vLLM+ baseline
+def _vllm(model, capb, capn, x):
+    return tg.Variant(model, capb, capn, 0, x)
+
+
+def test_vllm_occurrence_rule_on_gpu():
+    """PAPER:378 + PAPER:532: block checkpointing reuses a purely-input prefix from its
+    second occurrence, whole blocks only."""
+    P = list(range(7, 107))
+    tr = tg.from_sequences([(P, [900 + k, 901 + k]) for k in range(3)])
+    g, out = GU.gpu_grid(tr, [_vllm(tg.MODEL_7B, tg.UNLIMITED_BYTES, 0, 32)], [0.0], 1, max_nodes=64)
+    assert out["hit"].cpu().numpy()[0, 0].tolist() == [0, 96, 96]
+
+
+def test_vllm_micro_traces():
+    """Micro traces x block sizes 1..8 x byte / node capacities, two segments, two α
+    (ignored by the policy): snapshots, per-request hits and eviction logs vs the oracle."""
+    for seed in range(120):
+        tr = tg.micro_trace(seed, n_req=20, max_len=64, alphabet=2 + seed % 3)
+        model = tg.MODEL_7B if seed % 2 else tg.MODEL_TOY
+        x = 1 + seed % 8
+        bb = FL_KVT(model) * x + FL_SSMB(model)
+        k = seed % 3
+        capb, capn = ((tg.UNLIMITED_BYTES, 2 + seed % 7) if k == 0 else
+                      ((2 + seed % 5) * bb + seed % 7, 0) if k == 1 else ((3 + seed % 4) * bb, 3 + seed % 5))
+        v = _vllm(model, capb, capn, x)
+        alphas = [0.0, 1.0]
+        g, out = GU.gpu_grid(tr, [v], alphas, 2, max_nodes=128, log_cap=256, counters=True)
+        snaps, live, res, segs = GU.oracle_grid(tr, [v], alphas, 2, threads=1)
+        for kk in range(len(snaps[0])):
+            gs, gn = g.ctx.get_snapshot(0, kk)
+            assert gn == snaps[0][kk][1] and np.array_equal(GU.canon(gs), GU.canon(snaps[0][kk][0])), (seed, kk)
+        hit = out["hit"].cpu().numpy()
+        ctr = out["counters"].cpu().numpy()
+        for cid, (h, f, b, c) in res.items():
+            ai, si = cid // len(segs), cid % len(segs)
+            first, n, kk = segs[si]
+            assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h), (seed, cid)
+            assert np.array_equal(ctr[cid], c.astype(np.int64)), (seed, cid, ctr[cid], c)
+            _, _, _, lg = GU.oracle_chain_log(tr, v, alphas[ai], first, n, snaps[0][kk])
+            glog, gn = g.ctx.read_log(out, cid)
+            _assert_logs_equal(glog, gn, lg, f"vllm seed {seed}")
+        assert np.array_equal(hit[0, 0], hit[0, 1])  # α does not enter LRU
+
+
+def FL_KVT(m):
+    return m.n_attn * 2 * m.d_model * m.bytes_per_param
+
+
+def FL_SSMB(m):
+    return m.n_ssm * (m.d_model * m.d_state + m.conv_in * m.conv_kernel) * m.bytes_per_param
+
+
+@pytest.mark.parametrize("x", [16, 32, 64])
+def test_vllm_config3_reduced(x):
+    w = tg.workload(3, R=5000)
+    w.variants = [_vllm(tg.MODEL_7B, 60 * tg.GB, 0, x)]
+    w.alphas = (0.0,)
+    w.n_segments = 10
+    _compare_grid(w, log_cap=4096)
+
+
+def test_vllm_and_marconi_in_one_grid():
+    """Mixed policies in one context: the replay runs the Marconi chains and the vLLM+
+    chains as two launches; both match the oracle; Marconi's hit sum is compared too."""
+    w = tg.workload(3, R=4000)
+    w.variants = [tg.Variant(tg.MODEL_7B, 60 * tg.GB), _vllm(tg.MODEL_7B, 60 * tg.GB, 0, 32)]
+    w.alphas = (0.0, 0.5, 2.0)
+    w.n_segments = 8
+    _compare_grid(w)
+
+
+def test_vllm_config2_full():
+    w = tg.workload(2)
+    w.variants = [_vllm(v.model, v.capacity_bytes, v.capacity_nodes, 32) for v in w.variants]
+    w.alphas = (0.0,)
+    _compare_grid(w)
+
+
+def test_vllm_config4_reduced():
+    """SWEBench-shaped (32K-token contexts): ~1000 blocks per sequence, ~125 evictions
+    per request (the oracle's cost bounds the size: 600 requests, 4 segments)."""
+    w = tg.workload(4, R=600)
+    w.variants = [_vllm(tg.MODEL_7B, 60 * tg.GB, 0, 32)]
+    w.alphas = (0.0,)
+    w.n_segments = 4
+    _compare_grid(w)
