@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const mc_segment seg = P.segs[s];
     Chain C;
     chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes, P.smem_nodes);
+    // the policy is a compile-time constant in each instantiation
+    if (kPolicy == 0) { C.block = 0; C.mthr = 2; } else { C.mthr = 1; C.alpha = 0.0; }
     load_snapshot(C, P, &P.snap[v], seg.snapshot);
     mc_evict_rec* log = P.log ? P.log + (uint64_t)c * P.log_cap : nullptr;
     uint32_t* log_n = P.log ? P.log_n + c : nullptr;
