@@ -48,6 +48,11 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", type=int, default=3)
+    p.add_argument("--policy", default="marconi", choices=["marconi", "vllm"],
+                   help="vllm: the vLLM+ baseline (NEXT-2) on the same trace -- a sweep of block sizes x "
+                        "cache sizes as variants (alpha does not apply to its LRU)")
+    p.add_argument("--blocks", default="16,32,64,128", help="vLLM+ block sizes (tokens)")
+    p.add_argument("--caps-gb", default="30,60,90,120", help="vLLM+ cache sizes (GB)")
     p.add_argument("--requests", type=int, default=0, help="override R (testing only)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -131,28 +136,34 @@ def algorithmic_bytes(ctr: np.ndarray, n_req_replayed: int) -> int:
 # CPU oracle arms (the only places bench.py executes oracle/)
 # ----------------------------------------------------------------------------
 def oracle_sample(w, target_s: float, cores: int):
-    """A bounded sample of the same workload for the oracle: the first k segments x all α,
-    with k sized so the sample takes about target_s seconds on `cores` threads."""
+    """A bounded sample of the same workload for the oracle: the first k segments x all
+    (variant, α) chains, k sized so the sample takes about target_s seconds on `cores`
+    threads.  Returns (snapshots, chains, k); chain snapshot index = variant * k + segment."""
     import oracle as O
-    tr, v = w.trace, w.variants[0]
+    tr, v0 = w.trace, w.variants[0]
     W = w.window
-    # calibrate: single-thread time per request-replay on one α = 1 chain of segment 1
-    snaps, *_ = O.live_pass(tr, v, W, upto=W)
+    # calibrate: single-thread time per request-replay on one chain of segment 1
+    snaps, *_ = O.live_pass(tr, v0, W, upto=W)
     t0 = time.perf_counter()
-    O.run_chains(tr, [v], [(0, 1.0, W + 1, W, 1)], snaps, n_threads=1) if len(snaps) > 1 else None
+    O.run_chains(tr, [v0], [(0, w.alphas[-1], W + 1, W, 1)], snaps, n_threads=1) if len(snaps) > 1 else None
     per_req = max((time.perf_counter() - t0) / W, 1e-6)
-    na = len(w.alphas)
-    k = int(max(1, min(len(w.segments()), target_s * cores / (per_req * W * na))))
-    snaps, *_ = O.live_pass(tr, v, W, upto=min(k * W, tr.n_requests))
+    nchain_per_seg = len(w.alphas) * len(w.variants)
+    k = int(max(1, min(len(w.segments()), target_s * cores / (per_req * W * nchain_per_seg))))
     segs = w.segments()[:k]
-    chains = [(0, a, f, n, i) for a in w.alphas for i, (f, n) in enumerate(segs)]
-    return snaps, chains
+    all_snaps = []
+    for v in w.variants:
+        sv, *_ = O.live_pass(tr, v, W, upto=min(k * W, tr.n_requests))
+        sv = (sv + [sv[-1]] * k)[:k]  # pad (only segments < k are used)
+        all_snaps.extend(sv)
+    chains = [(vi, a, f, n, vi * k + i) for vi in range(len(w.variants)) for a in w.alphas
+              for i, (f, n) in enumerate(segs)]
+    return all_snaps, chains, k
 
 
 def run_oracle(w, snaps, chains, cores):
     import oracle as O
     t0 = time.perf_counter()
-    hit, fl, by, hs, ctr = O.run_chains(w.trace, [w.variants[0]], chains, snaps, n_threads=cores)
+    hit, fl, by, hs, ctr = O.run_chains(w.trace, w.variants, chains, snaps, n_threads=cores)
     dt = time.perf_counter() - t0
     n = sum(c[3] for c in chains)
     return n, dt
@@ -160,11 +171,11 @@ def run_oracle(w, snaps, chains, cores):
 
 def cpu_baseline(w, target_s):
     cores = os.cpu_count() or 1
-    snaps, chains = oracle_sample(w, target_s, cores)
+    snaps, chains, k = oracle_sample(w, target_s, cores)
     n, dt = run_oracle(w, snaps, chains, cores)
-    k = len(snaps)
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"first {k} of {len(w.segments())} segments x {len(w.alphas)} alphas = {len(chains)} chains, "
+            "sample": f"first {k} of {len(w.segments())} segments x {len(w.variants)} variant(s) x "
+                      f"{len(w.alphas)} alphas = {len(chains)} chains, "
                       f"{n} request-replays in {dt:.2f} s (snapshots from the oracle's own live pass, untimed)"}
 
 
@@ -173,7 +184,7 @@ def reference_arm(args, w, config):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    snaps, chains = oracle_sample(w, min(args.cpu_seconds, 8.0), cores)
+    snaps, chains, k = oracle_sample(w, min(args.cpu_seconds, 8.0), cores)
     for _ in range(args.warmup):
         run_oracle(w, snaps, chains, cores)
     tot_n, tot_t = 0, 0.0
@@ -187,7 +198,7 @@ def reference_arm(args, w, config):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
             "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{len(chains)} chains of the first {len(snaps)} segments per step"},
+                             "sample": f"{len(chains)} chains of the first {k} segments per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -202,16 +213,25 @@ def main():
     n_prob = max(1, world) if args.impl == "b200" else 1
     t_gen = time.perf_counter()
     ws = [tg.workload(args.config, R=args.requests or None, problem=k) for k in range(n_prob)]
+    if args.policy == "vllm":  # NEXT-2: the vLLM+ baseline on the same traces, block x cache-size sweep
+        blocks = [int(b) for b in args.blocks.split(",")]
+        caps = [int(float(c) * tg.GB) for c in args.caps_gb.split(",")]
+        for wk in ws:
+            m = wk.variants[0].model
+            wk.variants = [tg.Variant(m, c, 0, 0, b) for b in blocks for c in caps]
+            wk.alphas = (0.0,)
     t_gen = time.perf_counter() - t_gen
     w = ws[0]
     tr = w.trace
-    config = {"workload": f"config{args.config} {w.name}-shaped trace, {tr.n_requests} requests, "
+    pol = (f"vLLM+ baseline (state per token block, LRU; blocks {args.blocks} x caches {args.caps_gb} GB), "
+           if args.policy == "vllm" else "")
+    config = {"workload": f"config{args.config} {w.name}-shaped trace, {pol}{tr.n_requests} requests, "
                           f"{len(w.variants)} cache variant(s), {len(w.alphas)} alphas x {len(w.segments())} "
                           f"segments = {w.n_chains} chains" +
                           (f"; x {n_prob} independent problems (one per GPU, weak scaling)" if n_prob > 1 else ""),
               "requests": tr.n_requests, "tokens": tr.n_tokens, "alphas": len(w.alphas),
               "segments": len(w.segments()), "chains": w.n_chains * n_prob, "window": w.window,
-              "problems": n_prob,
+              "problems": n_prob, "policy": args.policy,
               "model": "7B hybrid {4 attn, 24 ssm, 28 mlp}, D=4096, N=128, fp16" if args.config in (2, 3, 4)
               else "see tracegen.workload", "cache_bytes": [v.capacity_bytes for v in w.variants],
               "l2": "flushed (256 MiB write) between timed steps, outside the event window"}
@@ -318,7 +338,8 @@ def main():
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            if tj.get("config") == args.config and tj.get("n_gpus", 1) == world:
+            if (tj.get("config") == args.config and tj.get("n_gpus", 1) == world
+                    and tj.get("policy", "marconi") == args.policy):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -343,7 +364,7 @@ def main():
                            setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "replay_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "kernel": "replay_kernel<%d>" % (args.policy == "vllm"), "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": kern_avg_s * 1000.0},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -367,12 +388,13 @@ def e2e_measure(gs, ws, args, outs):
         ctx = g.ctx
         h_tok = torch.from_numpy(np.ascontiguousarray(tr.tokens, np.uint32).view(np.int32)).pin_memory()
         h_req = torch.from_numpy(M.requests_array(tr.off, tr.lin, tr.lout).view(np.int64)).pin_memory()
-        snaps = [ctx.get_snapshot(0, k) for k in range(ctx.snapshot_count(0))]
+        snaps = [[ctx.get_snapshot(v, k) for k in range(ctx.snapshot_count(v))] for v in range(len(wk.variants))]
         d_tok = torch.empty_like(h_tok, device="cuda")
         d_req = torch.empty_like(h_req, device="cuda")
         h_hit = torch.empty(o["hit"].shape, dtype=torch.int32).pin_memory()
         st.append((g, tr, ctx, o, h_tok, h_req, snaps, d_tok, d_req, h_hit))
-    h2d = sum(x[4].numel() * 4 + x[5].numel() * 8 + sum(len(s[0]) for s in x[6]) * M.SNAP_DTYPE.itemsize for x in st)
+    h2d = sum(x[4].numel() * 4 + x[5].numel() * 8 + sum(len(s[0]) for sv in x[6] for s in sv) * M.SNAP_DTYPE.itemsize
+              for x in st)
     d2h = sum(x[9].numel() * 4 + x[3]["hit_sum"].numel() * 8 for x in st)
     n_units = sum(sum(n for _, n, _ in g.segs) * len(wk.alphas) * len(wk.variants) for g, wk in zip(gs, ws))
 
@@ -381,7 +403,8 @@ def e2e_measure(gs, ws, args, outs):
             d_tok.copy_(h_tok, non_blocking=True)
             d_req.copy_(h_req, non_blocking=True)
             ctx.set_trace_device(d_tok, d_req, tr.n_requests)
-            ctx.set_snapshots(0, snaps)
+            for v, sv in enumerate(snaps):
+                ctx.set_snapshots(v, sv)
             o["hit_sum"].zero_()
             g.run(out=o)
             h_hit.copy_(o["hit"], non_blocking=True)

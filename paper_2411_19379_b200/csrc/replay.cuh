@@ -138,14 +138,16 @@ struct KParams {
 
 // Per-worker workspace slice.  The caller zero-initialises the workspace once
 // (header word 0 = child-index generation, word 1 = layout signature).
+// Slice layout (byte offsets from the slice base; n = ncap, h = hcap):
+//   header 256 | records 32n | ids 4n | dslot 4n | path 4n | freel 4n | child index 16h |
+//   dense tail 8n | exact eff (f64) 8n
+// (n is a power of two >= 64, so every region stays 16 B aligned).  ws_bytes_per_worker
+// is the end of the last region, so the accessors below and the stride cannot disagree.
+__host__ __device__ inline uint64_t ws_off_tab(uint32_t n) { return 256 + 48ull * n; }
+__host__ __device__ inline uint64_t ws_off_tail(uint32_t n, uint32_t h) { return ws_off_tab(n) + 16ull * h; }
+__host__ __device__ inline uint64_t ws_off_eff(uint32_t n, uint32_t h) { return ws_off_tail(n, h) + 8ull * n; }
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
-  uint64_t b = 256                  // header
-               + 32ull * ncap       // node records
-               + 16ull * ncap       // node ids (4 B, padded so the child index is 16 B aligned)
-               + 16ull * hcap       // child index
-               + 12ull * ncap       // dslot, path, freel
-               + 8ull * ncap        // dense tail (positions >= S)
-               + 8ull * ncap;       // exact eff (f64) per dense position
+  const uint64_t b = ws_off_eff(ncap, hcap) + 8ull * ncap;
   return (b + 255) & ~255ull;
 }
 
@@ -154,13 +156,13 @@ struct WS {
   uint32_t n, h;
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
-  __device__ __forceinline__ HEnt* tab() const { return (HEnt*)(b + 256 + 48ull * n); }  // 16 B aligned
   __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
-  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 48ull * n + 16ull * h); }
-  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 52ull * n + 16ull * h); }
-  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 56ull * n + 16ull * h); }
-  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + 256 + 64ull * n + 16ull * h); }
-  __device__ __forceinline__ double* eff64() const { return (double*)(b + 256 + 72ull * n + 16ull * h); }
+  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n); }
+  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n); }
+  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n); }
+  __device__ __forceinline__ HEnt* tab() const { return (HEnt*)(b + ws_off_tab(n)); }
+  __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + ws_off_tail(n, h)); }
+  __device__ __forceinline__ double* eff64() const { return (double*)(b + ws_off_eff(n, h)); }
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -1423,6 +1425,14 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   // Step 2: hit = the deepest matched block end <= L_in (V4).
   const uint32_t reuse = min(mb, L_in / x) * x;
 
+#ifdef MC_DEBUG
+  for (uint32_t i = lane; i < mb; i += 32) {
+    const uint32_t sl = path[i];
+    if (sl >= C.hwm || C.w.rec()[sl].dpos >= C.count)
+      printf("vllm walk: r %u k %u/%u slot %u hwm %u dpos %u count %u nb %u S %u\n", r, i, mb, sl, C.hwm,
+             sl < C.ncap ? C.w.rec()[sl].dpos : 0u, C.count, nb, C.S);
+  }
+#endif
   // Step 3: touch (t_last = r) and pin every matched block (V5, V7), in parallel.
   for (uint32_t i = lane; i < mb; i += 32) {
     DenseRec* d = d_ptr(C, C.w.rec()[path[i]].dpos);

@@ -1,3 +1,2 @@
 #!/bin/bash
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "vllm or config3_reduced_full" 2>&1 | tail -2
-NOTEST=1 ./run_variants.sh
+for m in 8192 4096 2048 8192 4096 2048; do MAXN=$m timeout 300 python tools/variant_timing.py 2>&1 | tail -1 | sed "s/^/MAXN=$m /"; done

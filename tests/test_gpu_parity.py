@@ -533,3 +533,15 @@ def test_vllm_config4_reduced():
     w.alphas = (0.0,)
     w.n_segments = 4
     _compare_grid(w)
+
+
+def test_dense_positions_beyond_half_the_node_table():
+    """Regression: live counts above max_nodes/2 on concurrent workers (the exact-eff array
+    of one worker slice used to overrun into the next slice)."""
+    w = tg.workload(3, R=3000)
+    w.n_segments = 8
+    w.alphas = (0.0, 1.0, 4.0)
+    _compare_grid(w, R_cap_nodes=2048)
+    w.variants = [_vllm(tg.MODEL_7B, 120 * tg.GB, 0, 16)]
+    w.alphas = (0.0,)
+    _compare_grid(w)
