@@ -337,10 +337,10 @@ def main():
     tp = os.path.join(ROOT, "profiles", "replay_traffic.json")
     if os.path.exists(tp):
         try:
-            tj = json.load(open(tp))
-            if (tj.get("config") == args.config and tj.get("n_gpus", 1) == world
-                    and tj.get("policy", "marconi") == args.policy):
-                traffic = tj.get("dram_bytes_per_launch")
+            for tj in json.load(open(tp)):  # one entry per (config, n_gpus, policy) capture
+                if (tj.get("config") == args.config and tj.get("n_gpus", 1) == world
+                        and tj.get("policy", "marconi") == args.policy):
+                    traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
