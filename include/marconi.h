@@ -209,6 +209,15 @@ typedef struct {
  * replays its window at its α and writes per-request outputs and its hit sum. */
 mc_status mc_replay(mc_ctx* ctx, const mc_replay_args* args, void* stream);
 
+/* Copy one chain's eviction log of an mc_replay call to the host (SURVEY.md §8(b)
+ * mc_eviction_log).  `args` = the arguments of that call (d_log, d_log_n, log_cap and
+ * n_alpha are used); chain = ((variant * n_alpha) + alpha_idx) * n_segs + seg.
+ * Synchronises `stream` first.  *n_out = evictions the chain made in that call (may
+ * exceed log_cap: only the first log_cap were recorded); h_out (nullable) receives
+ * min(*n_out, log_cap, cap) records in eviction order.  MC_EINVAL if the call had no log. */
+mc_status mc_eviction_log(mc_ctx* ctx, const mc_replay_args* args, uint32_t variant, uint32_t alpha_idx,
+                          uint32_t seg, mc_evict_rec* h_out, uint64_t cap, uint64_t* n_out, void* stream);
+
 /* Synchronise `stream` and map the device status word to an mc_status. */
 mc_status mc_check(mc_ctx* ctx, void* stream);
 

@@ -715,6 +715,24 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   return MC_OK;
 }
 
+mc_status mc_eviction_log(mc_ctx* c, const mc_replay_args* A, uint32_t v, uint32_t a, uint32_t s,
+                          mc_evict_rec* h_out, uint64_t cap, uint64_t* n_out, void* stream) {
+  if (!c || !A || !n_out) return fail(MC_EINVAL, "mc_eviction_log: null argument");
+  if (!A->d_log || !A->d_log_n) return fail(MC_EINVAL, "mc_eviction_log: the replay call had no log buffers");
+  const uint32_t nv = (uint32_t)c->hv.size(), ns = (uint32_t)c->segs.size();
+  if (v >= nv || a >= A->n_alpha || s >= ns) return fail(MC_EINVAL, "mc_eviction_log: chain out of range");
+  const uint64_t chain = ((uint64_t)v * A->n_alpha + a) * ns + s;
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  uint32_t n = 0;
+  CU(cudaMemcpy(&n, A->d_log_n + chain, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  *n_out = n;
+  if (h_out) {
+    const uint64_t k = std::min<uint64_t>(std::min<uint64_t>(n, A->log_cap), cap);
+    if (k) CU(cudaMemcpy(h_out, A->d_log + chain * A->log_cap, k * sizeof(mc_evict_rec), cudaMemcpyDeviceToHost));
+  }
+  return MC_OK;
+}
+
 mc_status mc_check(mc_ctx* c, void* stream) {
   if (!c) return fail(MC_EINVAL, "mc_check: null context");
   CU(cudaStreamSynchronize((cudaStream_t)stream));

@@ -28,7 +28,7 @@ assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYP
 EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at",
             "mc_snapshot_count",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
-            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin")
+            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log")
 
 MC_STATUS = {0: "MC_OK", -1: "MC_EINVAL", -2: "MC_ENOMEM", -3: "MC_ECUDA", -4: "MC_EOVERFLOW",
              -5: "MC_ESTATE", -6: "MC_EDEVICE"}
@@ -84,6 +84,7 @@ def lib():
             "mc_workspace_workers": [P, U64, U32, U32, P],
             "mc_replay": [P, P, P],
             "mc_check": [P, P],
+            "mc_eviction_log": [P, P, U32, U32, U32, P, U64, P, P],
             "mc_node_cost": [P, U32, P, P, P, P, P, P, P],
             "mc_score_argmin": [U32, P, P, P, P, P, P, P, P, P],
         }.items():
@@ -323,6 +324,22 @@ class Context:
 
     def check(self, stream=None):
         check(lib().mc_check(self.h, _stream_ptr(stream)))
+
+    def eviction_log(self, out, n_alpha: int, variant: int, alpha_idx: int, seg: int, stream=None):
+        """One chain's eviction log through the C ABI (mc_eviction_log): (records, n_evictions)."""
+        a = mc_replay_args()
+        a.n_alpha = n_alpha
+        a.d_log = out["log"].data_ptr()
+        a.d_log_n = out["log_n"].data_ptr()
+        a.log_cap = out["log_cap"]
+        n = C.c_uint64()
+        check(lib().mc_eviction_log(self.h, C.byref(a), variant, alpha_idx, seg, None, 0, C.byref(n),
+                                    _stream_ptr(stream)))
+        k = min(n.value, out["log_cap"])
+        rec = np.zeros(k, EVICT_DTYPE)
+        check(lib().mc_eviction_log(self.h, C.byref(a), variant, alpha_idx, seg, _np_ptr(rec), k, C.byref(n),
+                                    _stream_ptr(stream)))
+        return rec, n.value
 
     @staticmethod
     def read_log(out, chain: int) -> np.ndarray:

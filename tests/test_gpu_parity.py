@@ -226,7 +226,14 @@ def _compare_grid(w, R_cap_nodes=8192, log_cap=0, threads=0):
 def test_config3_reduced_full_parity():
     w = tg.workload(3, R=4000)
     w.n_segments = 8
-    _compare_grid(w, log_cap=4096)
+    g, out = _compare_grid(w, log_cap=4096)
+    # the same logs through the C ABI call (mc_eviction_log) as through the raw buffers
+    na, ns = len(w.alphas), len(g.segs)
+    for ai in (0, na // 2, na - 1):
+        for si in (0, ns - 1):
+            rec, n = g.ctx.eviction_log(out, na, 0, ai, si)
+            raw, n2 = g.ctx.read_log(out, ai * ns + si)
+            assert n == n2 and np.array_equal(rec.view(np.uint8), raw.view(np.uint8))
 
 
 def test_config2_reduced():
