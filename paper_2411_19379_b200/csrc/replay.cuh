@@ -579,6 +579,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     E.roff = R.roff;
   }
   __syncwarp();
+  bool bad_t = false;
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
@@ -586,11 +587,15 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     C.w.eff64()[i] = v;
     DenseRec* d = d_ptr(C, i);
     d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
-    d->e32 = __double2float_rn(v);
+    // vLLM+ keeps the node id in the second dense word (LRU key (t, id)); Marconi RN32(eff)
+    d->e32 = C.block ? __uint_as_float(nodes[i].id) : __double2float_rn(v);
+    // vLLM+ trees keep t_last(parent) >= t_last(child) (whole paths are touched); the
+    // batched LRU eviction relies on it, so a snapshot violating it is rejected
+    if (C.block && pidx[i] != NIL && nodes[pidx[i]].t_last < nodes[i].t_last) bad_t = true;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(FULL, (unsigned long long)bytes, o);
-  if (__any_sync(FULL, bad)) {
+  if (__any_sync(FULL, bad || bad_t)) {
     if (lane == 0) atomicOr(P.status, ST_INVARIANT);
     C.failed = true;
   }
@@ -1382,6 +1387,145 @@ __device__ __forceinline__ uint32_t child_block(const Chain& C, const KParams& P
   return NIL;
 }
 
+// vLLM+ LRU eviction of `need` leaf blocks (V6), batched: one scan keeps each lane's
+// K smallest candidate keys (t_last << 32 | id) and W = a lower bound of every key not
+// kept; victims are then extracted in exact (t, id) order while the smallest kept key is
+// below W.  A removal can expose the parent as a new candidate (its last child gone):
+// it joins the kept keys (or is covered by W).  Because whole paths are touched, t(parent)
+// >= t(child) and the global t minimum is always the victim's, so the logged utility
+// (Eq. 2 at α = 0) is 0, or 0.5 when every node shares t.  Same victims, order, log and
+// counters as one full scan per eviction.
+__device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_t need, mc_evict_rec* log,
+                                 uint32_t* log_n) {
+  constexpr int K = 4;
+  const uint64_t INF64 = ~0ull;
+  const uint32_t lane = lane_id();
+  while (need && !C.failed) {
+    uint64_t key[K];
+    uint32_t pos[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) { key[q] = INF64; pos[q] = NIL; }
+    uint64_t wl = INF64;
+    uint32_t tmax = 0;
+    scan_dense(C, C.count, [&](int, uint32_t i, uint32_t tc, float e) {
+      tmax = max(tmax, tc & T_MASK);
+      if (tc & D_FLAGS) return;
+      const uint64_t k = ((uint64_t)(tc & T_MASK) << 32) | __float_as_uint(e);
+      if (k < key[K - 1]) {
+        wl = min(wl, key[K - 1]);  // the dropped key (INF64 while the list is not full)
+        key[K - 1] = k;
+        pos[K - 1] = i;
+#pragma unroll
+        for (int q = K - 1; q > 0; q--) {
+          if (key[q] < key[q - 1]) {
+            const uint64_t tk = key[q]; key[q] = key[q - 1]; key[q - 1] = tk;
+            const uint32_t tp = pos[q]; pos[q] = pos[q - 1]; pos[q - 1] = tp;
+          }
+        }
+      } else {
+        wl = min(wl, k);
+      }
+    });
+    uint64_t W = wl;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      W = min(W, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)W, o));
+      tmax = max(tmax, __shfl_xor_sync(FULL, tmax, o));
+    }
+    bool progressed = false;
+    while (need) {
+      uint64_t m = key[0];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = min(m, (uint64_t)__shfl_xor_sync(FULL, (unsigned long long)m, o));
+      if (m == INF64 || m >= W) break;  // the next victim may be unlisted: rescan
+      const int src = __ffs(__ballot_sync(FULL, key[0] == m)) - 1;
+      const uint32_t vpos = __shfl_sync(FULL, pos[0], src);
+      if (lane == src) {
+#pragma unroll
+        for (int q = 0; q < K - 1; q++) { key[q] = key[q + 1]; pos[q] = pos[q + 1]; }
+        key[K - 1] = INF64;
+        pos[K - 1] = NIL;
+      }
+      const uint32_t cnt = C.count, last = cnt - 1;
+      const uint32_t t_v = (uint32_t)(m >> 32);
+      uint32_t e_pos = NIL;
+      uint64_t e_key = INF64;
+      if (lane == 0) {
+        const uint32_t x = d_slot(C, vpos);
+        const uint32_t sl = d_slot(C, last);
+        const NodeRec X = C.w.rec()[x];
+        const uint32_t p = X.parent;
+        const NodeRec Rp = C.w.rec()[p];
+        C.total -= node_bytes(C.m, X.ds, X.de, (X.nf >> 24) & F_SSM);
+        hash_erase_at_1(C, X.hidx);
+        NodeRec& Wp = C.w.rec()[p];
+        Wp.nf = Rp.nf - 1;
+        Wp.cxor = Rp.cxor ^ x;
+        if (p != 0) d_multi(C, Rp.dpos, (Rp.nf & NCH_MASK) - 1);
+        if (log) {
+          const uint32_t li = *log_n;
+          if (li < P.log_cap) {
+            mc_evict_rec e;
+            e.req = r; e.node_id = (uint32_t)m; e.kind = 0; e.n_live = cnt;
+            e.utility = (t_v == tmax) ? 0.5 : 0.0;  // (t - tmin)/(tmax - tmin) with tmin = t_v
+            log[li] = e;
+          }
+          *log_n = li + 1;
+        }
+        if (vpos != last) {
+          *d_ptr(C, vpos) = *d_ptr(C, last);
+          d_set_slot(C, vpos, sl);
+          C.w.rec()[sl].dpos = vpos;
+        }
+        C.count = last;
+        C.w.rec()[x].nf = 0;
+        C.w.freel()[C.nfree++] = x;
+        C.c_wr += 1;
+        if (p != 0 && (Rp.nf & NCH_MASK) == 1) {  // the parent lost its last child
+          const uint32_t pp = (Rp.dpos == last) ? vpos : Rp.dpos;
+          const DenseRec dp = *d_ptr(C, pp);
+          if (!(dp.tc & D_FLAGS)) {
+            e_pos = pp;
+            e_key = ((uint64_t)(dp.tc & T_MASK) << 32) | __float_as_uint(dp.e32);
+          }
+        }
+      }
+      sync_state(C);
+      C.c_scan += cnt;
+      C.n_evict++;
+      need--;
+      progressed = true;
+      // the entry that moved from `last` into the victim's position keeps its listing
+#pragma unroll
+      for (int q = 0; q < K; q++)
+        if (pos[q] == last) pos[q] = vpos;
+      e_pos = __shfl_sync(FULL, e_pos, 0);
+      e_key = __shfl_sync(FULL, (unsigned long long)e_key, 0);
+      if (e_pos != NIL && e_key < W) {  // keep the exposed parent (else W covers it)
+        if (lane == (e_pos & 31u)) {
+          const uint64_t dropped = key[K - 1];
+          key[K - 1] = e_key;
+          pos[K - 1] = e_pos;
+#pragma unroll
+          for (int q = K - 1; q > 0; q--) {
+            if (key[q] < key[q - 1]) {
+              const uint64_t tk = key[q]; key[q] = key[q - 1]; key[q - 1] = tk;
+              const uint32_t tp = pos[q]; pos[q] = pos[q - 1]; pos[q - 1] = tp;
+            }
+          }
+          wl = dropped;
+        }
+        const uint64_t d = __shfl_sync(FULL, (unsigned long long)wl, e_pos & 31u);
+        W = min(W, d);
+      }
+    }
+    if (!progressed && need) {  // no candidate at all
+      if (lane == 0) atomicOr(P.status, ST_NOCAND);
+      C.failed = true;
+    }
+  }
+}
+
 __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, const Prefetched cur,
                                        Prefetched& nxt, bool has_next, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
@@ -1447,9 +1591,12 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   const uint64_t d_bytes = bb * n_new;
   const bool bypass = (bb * mb + d_bytes > C.capb) || (C.capn && nb > C.capn);
   if (!bypass) {
-    // Step 5: LRU leaf eviction (V6) until the new blocks fit.
-    while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + n_new > C.capn)))
-      evict_one(C, P, r, log, log_n);
+    // Step 5: LRU leaf eviction (V6) until the new blocks fit; every block has the same
+    // size, so the number of victims is known up front.
+    uint64_t need = 0;
+    if (C.total + d_bytes > C.capb) need = (C.total + d_bytes - C.capb + bb - 1) / bb;
+    if (C.capn && C.count + n_new > C.capn) need = max(need, (uint64_t)(C.count + n_new - C.capn));
+    if (need) evict_lru_blocks(C, P, r, (uint32_t)need, log, log_n);
     // Step 6: insert blocks mb .. nb-1 under v, in parallel (one block per lane).
     if (n_new && !C.failed) {
       const uint32_t take = min(C.nfree, n_new);
@@ -1490,10 +1637,9 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           C.w.rec()[s] = R;
           C.w.ids()[s] = id0 + j;
           d_set_slot(C, cnt0 + j, s);
-          C.w.eff64()[cnt0 + j] = 0.0;  // unused by LRU
           DenseRec* d = d_ptr(C, cnt0 + j);
           d->tc = r | (inner ? D_MULTI : 0u);
-          d->e32 = 0.0f;
+          d->e32 = __uint_as_float(id0 + j);  // vLLM+: the id, so (t, id) LRU keys need no global read
         }
         if (lane == 0) {
           NodeRec& Rv = C.w.rec()[v];
