@@ -72,7 +72,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes, P.smem_nodes);
     // the policy is a compile-time constant in each instantiation
     if (kPolicy == 0) { C.block = 0; C.mthr = 2; } else { C.mthr = 1; C.alpha = 0.0; }
-    load_snapshot(C, P, &P.snap[v], seg.snapshot);
+#ifdef MC_LOAD_TIMER
+    const long long _l0 = clock64();
+#endif
+    load_image(C, P, P.snap[v].img + P.snap[v].img_off[seg.snapshot]);
+#ifdef MC_LOAD_TIMER
+    const long long _l1 = clock64();
+#endif
     mc_evict_rec* log = P.log ? P.log + (uint64_t)c * P.log_cap : nullptr;
     uint32_t* log_n = P.log ? P.log_n + c : nullptr;
     if (lane == 0 && log_n) *log_n = 0;
@@ -104,11 +110,28 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
         P.counters[4ull * c + 1] = C.c_vis;
         P.counters[4ull * c + 2] = C.c_scan;
         P.counters[4ull * c + 3] = C.c_wr;
+#ifdef MC_LOAD_TIMER
+        P.counters[4ull * c + 0] = (unsigned long long)(_l1 - _l0);
+#endif
 #endif
       }
       if (P.chain_cycles) P.chain_cycles[c] = (uint32_t)min((long long)0xFFFFFFFF, (clock64() - t0) >> 10);
     }
     __syncwarp();
+  }
+}
+
+// Snapshot images (setup): warp w builds the images of snapshots w, w + n_workers, ...
+// of variant `v` by running load_snapshot on its scratch slice (whole dense list in the
+// global tail) and exporting the result.
+__global__ void __launch_bounds__(32) image_kernel(KParams P, uint32_t v, char* img, const uint64_t* img_off) {
+  const uint32_t w = blockIdx.x;
+  const DevSnapStore& st = P.snap[v];
+  for (uint32_t k = w; k < st.count; k += P.n_workers) {
+    Chain C;
+    chain_init(C, P, w, P.var[v], 0.0, nullptr, 0);
+    load_snapshot(C, P, &st, k);
+    export_image(C, img + img_off[k]);
   }
 }
 
@@ -217,8 +240,11 @@ struct SnapStore {
   uint32_t* nid = nullptr;
   uint32_t count = 0;
   uint64_t cap = 0;
+  char* img = nullptr;          // snapshot images (ImgHdr layout), rebuilt whenever the store changes
+  uint64_t* img_off = nullptr;
   void release() {
     cudaFree(nodes); cudaFree(pidx); cudaFree(off); cudaFree(n); cudaFree(nid);
+    cudaFree(img); cudaFree(img_off);
     *this = SnapStore();
   }
 };
@@ -277,6 +303,8 @@ mc_status upload_stores(mc_ctx* c) {
     h[v].off = c->snaps[v].off;
     h[v].n = c->snaps[v].n;
     h[v].nid = c->snaps[v].nid;
+    h[v].img = c->snaps[v].img;
+    h[v].img_off = c->snaps[v].img_off;
     h[v].count = c->snaps[v].count;
     h[v].pad = 0;
   }
@@ -285,6 +313,56 @@ mc_status upload_stores(mc_ctx* c) {
 }
 
 uint32_t default_workers(const mc_ctx* c) { return (uint32_t)(c->n_sm * c->blocks_per_sm * kWarpsPerCta); }
+
+// (Re)build the loadable images of variant v's snapshots (setup-time; allocates).
+mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st) {
+  SnapStore& s = c->snaps[v];
+  cudaFree(s.img);
+  cudaFree(s.img_off);
+  s.img = nullptr;
+  s.img_off = nullptr;
+  if (s.count == 0) return upload_stores(c);
+  std::vector<uint32_t> n(s.count);
+  CU(cudaMemcpyAsync(n.data(), s.n, sizeof(uint32_t) * s.count, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::vector<uint64_t> off(s.count + 1, 0);
+  for (uint32_t k = 0; k < s.count; k++) {
+    if (n[k] + 1 > c->ncap) return fail(MC_EOVERFLOW, "snapshot larger than max_nodes");
+    off[k + 1] = off[k] + ((img_bytes(n[k]) + 255) & ~255ull);
+  }
+  if (cudaMalloc(&s.img, off[s.count]) != cudaSuccess ||
+      cudaMalloc(&s.img_off, sizeof(uint64_t) * (s.count + 1)) != cudaSuccess)
+    return fail(MC_ENOMEM, "snapshot image allocation failed");
+  CU(cudaMemcpyAsync(s.img_off, off.data(), sizeof(uint64_t) * (s.count + 1), cudaMemcpyHostToDevice, st));
+  mc_status rc = upload_stores(c);
+  if (rc != MC_OK) return rc;
+  const uint32_t nb = std::min<uint32_t>(s.count, 4u * (uint32_t)c->n_sm);
+  const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
+  char* scratch = nullptr;
+  if (cudaMalloc(&scratch, per * nb) != cudaSuccess) return fail(MC_ENOMEM, "image scratch allocation failed");
+  CU(cudaMemsetAsync(scratch, 0, per * nb, st));  // slices start zeroed (generation header)
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.tok = c->tok;
+  P.n_tok = c->n_tok;
+  P.req = c->req;
+  P.n_req = c->n_req;
+  P.n_var = (uint32_t)c->hv.size();
+  P.var = c->d_var;
+  P.snap = c->d_stores;
+  P.ncap = c->ncap;
+  P.hcap = c->hcap;
+  P.n_workers = nb;
+  P.ws = scratch;
+  P.ws_stride = per;
+  P.status = c->d_status;
+  image_kernel<<<nb, 32, 0, st>>>(P, v, s.img, s.img_off);
+  const cudaError_t e = cudaGetLastError();
+  cudaStreamSynchronize(st);
+  cudaFree(scratch);
+  if (e != cudaSuccess) return fail(MC_ECUDA, std::string("image_kernel: ") + cudaGetErrorString(e));
+  return MC_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -466,7 +544,9 @@ mc_status mc_set_snapshots(mc_ctx* c, uint32_t variant, const mc_snap_node* h_no
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(st));
   s.count = n_snap;
-  return upload_stores(c);
+  mc_status rc = upload_stores(c);
+  if (rc != MC_OK) return rc;
+  return build_images(c, variant, st);
 }
 
 mc_status mc_workspace_size(const mc_ctx* c, uint32_t n_workers, uint32_t n_alpha, uint32_t n_chains,
@@ -564,7 +644,9 @@ mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points
   if (h_first_evict)
     CU(cudaMemcpyAsync(h_first_evict, c->d_points + K, sizeof(uint32_t) * nv, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  return upload_stores(c);
+  mc_status rc = upload_stores(c);
+  for (uint32_t v = 0; v < nv && rc == MC_OK; v++) rc = build_images(c, v, st);
+  return rc;
 }
 
 mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,

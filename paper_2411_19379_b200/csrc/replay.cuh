@@ -80,8 +80,32 @@ struct DevSnapStore {
   const uint64_t* off;
   const uint32_t* n;
   const uint32_t* nid;
+  const char* img;         // loadable images of the snapshots (see ImgHdr), built at setup
+  const uint64_t* img_off; // byte offset of snapshot k's image
   uint32_t count, pad;
 };
+
+// Snapshot image: a chain's workspace state right after loading the snapshot, built once
+// per snapshot at setup (image_kernel) so the 16+ chains that start from the same
+// snapshot copy it (coalesced, no child-index CAS, no Eq. 1 divisions) instead of
+// rebuilding it.  Byte layout from the image base (n = nodes):
+//   ImgHdr 64 | records 32(n+1) | ids 4(n+1) | dslot 4n | dense 8n | exact eff 8n |
+//   child-index positions 4n | child-index entries 16n      (regions 16 B aligned)
+struct ImgHdr {
+  unsigned long long total;
+  uint32_t n, nid, tmin, tmax;
+  float lo32, hi32;
+  double elo, ehi;
+  uint32_t bc_valid, pad0, pad1, pad2;
+};
+__host__ __device__ inline uint64_t img_al16(uint64_t x) { return (x + 15) & ~15ull; }
+__host__ __device__ inline uint64_t img_off_ids(uint32_t n) { return 64 + 32ull * (n + 1); }
+__host__ __device__ inline uint64_t img_off_dslot(uint32_t n) { return img_off_ids(n) + img_al16(4ull * (n + 1)); }
+__host__ __device__ inline uint64_t img_off_dense(uint32_t n) { return img_off_dslot(n) + img_al16(4ull * n); }
+__host__ __device__ inline uint64_t img_off_eff(uint32_t n) { return img_off_dense(n) + img_al16(8ull * n); }
+__host__ __device__ inline uint64_t img_off_tpos(uint32_t n) { return img_off_eff(n) + img_al16(8ull * n); }
+__host__ __device__ inline uint64_t img_off_tent(uint32_t n) { return img_off_tpos(n) + img_al16(4ull * n); }
+__host__ __device__ inline uint64_t img_bytes(uint32_t n) { return img_off_tent(n) + 16ull * n; }
 // Writable view used by the live pass.
 struct DevSnapOut {
   mc_snap_node* nodes;
@@ -609,6 +633,198 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
 }
 
 // Live pass: write the current tree as snapshot k (dense order, parent positions).
+// Write the state load_snapshot just built (with S = 0: the whole dense list in the
+// global tail) as a snapshot image at dst, including the exact normalisation bounds a
+// first victim selection would compute (so chains start with the bound cache valid).
+__device__ void export_image(Chain& C, char* dst) {
+  const uint32_t lane = lane_id();
+  const uint32_t n = C.count;
+  uint32_t tmn = 0xFFFFFFFFu, tmx = 0;
+  float lo = __int_as_float(0x7F800000), hi = 0.0f;
+  double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
+  const DenseRec* dense = C.w.tail();
+  const double* e64 = C.w.eff64();
+  for (uint32_t i = lane; i < n; i += 32) {
+    const DenseRec d = dense[i];
+    const uint32_t t = d.tc & T_MASK;
+    tmn = min(tmn, t);
+    tmx = max(tmx, t);
+    lo = fminf(lo, d.e32);
+    hi = fmaxf(hi, d.e32);
+    const double e = e64[i];
+    elo = e < elo ? e : elo;
+    ehi = e > ehi ? e : ehi;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    tmn = min(tmn, __shfl_xor_sync(FULL, tmn, o));
+    tmx = max(tmx, __shfl_xor_sync(FULL, tmx, o));
+    lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+    const double a = __shfl_xor_sync(FULL, elo, o), b = __shfl_xor_sync(FULL, ehi, o);
+    elo = a < elo ? a : elo;
+    ehi = b > ehi ? b : ehi;
+  }
+  // records, ids, dslot, dense, eff
+  NodeRec* rec = (NodeRec*)(dst + 64);
+  uint32_t* ids = (uint32_t*)(dst + img_off_ids(n));
+  uint32_t* dsl = (uint32_t*)(dst + img_off_dslot(n));
+  DenseRec* dn = (DenseRec*)(dst + img_off_dense(n));
+  double* ef = (double*)(dst + img_off_eff(n));
+  for (uint32_t i = lane; i <= n; i += 32) {
+    rec[i] = C.w.rec()[i];
+    ids[i] = C.w.ids()[i];
+  }
+  for (uint32_t i = lane; i < n; i += 32) {
+    dsl[i] = C.w.dslot()[i];
+    dn[i] = dense[i];
+    ef[i] = e64[i];
+  }
+  // occupied child-index slots of this generation, compacted in slot order
+  uint32_t* tpos = (uint32_t*)(dst + img_off_tpos(n));
+  HEnt* tent = (HEnt*)(dst + img_off_tent(n));
+  uint32_t w = 0;
+  for (uint32_t base = 0; base <= C.hmask; base += 32) {
+    const uint32_t j = base + lane;
+    const HEnt e = C.w.tab()[j];
+    const bool occ = hvalid(C, e.key);
+    const unsigned b = __ballot_sync(FULL, occ);
+    if (occ) {
+      const uint32_t k = w + __popc(b & ((1u << lane) - 1u));
+      tpos[k] = j;
+      tent[k] = e;
+    }
+    w += __popc(b);
+  }
+  if (lane == 0) {
+    ImgHdr h;
+    h.total = C.total;
+    h.n = n;
+    h.nid = C.next_id;
+    h.tmin = tmn; h.tmax = tmx;
+    h.lo32 = lo; h.hi32 = hi;
+    h.elo = elo; h.ehi = ehi;
+    h.bc_valid = (n > 0 && w == n && !C.failed) ? 1u : 0u;
+    h.pad0 = w; h.pad1 = 0; h.pad2 = (C.failed || w != n) ? 1u : 0u;  // pad2: unusable image
+    *(ImgHdr*)dst = h;
+  }
+  __syncwarp();
+}
+
+#ifndef MC_COPY_UNROLL
+#define MC_COPY_UNROLL 1
+#endif
+constexpr int kCopyU = MC_COPY_UNROLL;  // loads in flight per lane in the image copies
+// Warp copy of n 16-byte words with kCopyU loads in flight per lane (latency-bound otherwise).
+__device__ __forceinline__ void warp_copy16(uint4* __restrict__ d, const uint4* __restrict__ s, uint32_t n) {
+  const uint32_t lane = lane_id();
+  for (uint32_t b = 0; b < n; b += 32 * kCopyU) {
+    uint4 v[kCopyU];
+#pragma unroll
+    for (int q = 0; q < kCopyU; q++) {
+      const uint32_t i = b + 32 * q + lane;
+      if (i < n) v[q] = __ldcs(s + i);
+    }
+#pragma unroll
+    for (int q = 0; q < kCopyU; q++) {
+      const uint32_t i = b + 32 * q + lane;
+      if (i < n) d[i] = v[q];
+    }
+  }
+}
+
+// The copies of load_image, out of line: its unrolled loads need registers the replay
+// loop's allocation should not pay for (plain arguments, so the Chain stays in registers).
+__device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S, const char* __restrict__ src,
+                                        uint32_t n, uint32_t g) {
+  const uint32_t lane = lane_id();
+  // records + ids + dslot are contiguous in the image but not in the slice
+  warp_copy16((uint4*)w.rec(), (const uint4*)(src + 64), 2 * (n + 1));
+  warp_copy16((uint4*)w.ids(), (const uint4*)(src + img_off_ids(n)), (uint32_t)(img_al16(4ull * (n + 1)) / 16));
+  warp_copy16((uint4*)w.dslot(), (const uint4*)(src + img_off_dslot(n)), (uint32_t)(img_al16(4ull * n) / 16));
+  warp_copy16((uint4*)w.eff64(), (const uint4*)(src + img_off_eff(n)), (n + 1) / 2);
+  {
+    const uint32_t ns = min(n, S);
+    const DenseRec* dn = (const DenseRec*)(src + img_off_dense(n));
+    for (uint32_t b = 0; b < n; b += 32 * kCopyU) {  // SMEM part and global tail
+      DenseRec v[kCopyU];
+#pragma unroll
+      for (int q = 0; q < kCopyU; q++) {
+        const uint32_t i = b + 32 * q + lane;
+        if (i < n) v[q] = dn[i];
+      }
+#pragma unroll
+      for (int q = 0; q < kCopyU; q++) {
+        const uint32_t i = b + 32 * q + lane;
+        if (i < n) *(i < ns ? sd + i : w.tail() + i) = v[q];
+      }
+    }
+  }
+  {
+    const uint32_t* tpos = (const uint32_t*)(src + img_off_tpos(n));
+    const HEnt* tent = (const HEnt*)(src + img_off_tent(n));
+    for (uint32_t b = 0; b < n; b += 32 * kCopyU) {
+      HEnt e[kCopyU];
+      uint32_t tp[kCopyU];
+#pragma unroll
+      for (int q = 0; q < kCopyU; q++) {
+        const uint32_t i = b + 32 * q + lane;
+        if (i < n) { e[q] = tent[i]; tp[q] = tpos[i]; }
+      }
+#pragma unroll
+      for (int q = 0; q < kCopyU; q++) {
+        const uint32_t i = b + 32 * q + lane;
+        if (i < n) {
+          e[q].key = (e[q].key & 0x0FFFFFFFu) | (g << 28);
+          w.tab()[tp[q]] = e[q];
+        }
+      }
+    }
+  }
+}
+
+// A chain's initial state from a snapshot image (replaces load_snapshot on the replay
+// path): bump the child-index generation, copy the image, re-tag the copied entries.
+__device__ void load_image(Chain& C, const KParams& P, const char* src) {
+  const uint32_t lane = lane_id();
+  const ImgHdr h = *(const ImgHdr*)src;
+  const uint32_t n = h.n;
+  if (n + 1 > C.ncap || h.pad2) {
+    if (lane == 0) atomicOr(P.status, h.pad2 ? ST_INVARIANT : ST_OVERFLOW);
+    C.failed = true;
+    return;
+  }
+  uint32_t g = 0;
+  bool clear = false;
+  if (lane == 0) {
+    uint32_t* hd = C.w.hdr();
+    g = hd[0] + 1;
+    if (g > GEN_MAX || hd[1] != C.ncap) {
+      clear = true;
+      g = 1;
+      hd[1] = C.ncap;
+    }
+    hd[0] = g;
+  }
+  g = __shfl_sync(FULL, g, 0);
+  clear = __shfl_sync(FULL, (int)clear, 0);
+  if (clear)
+    for (uint32_t i = lane; i <= C.hmask; i += 32) C.w.tab()[i].key = 0;
+  C.gen = g;
+  __syncwarp();
+  copy_image(C.w, C.sd, C.S, src, n, g);
+  C.total = h.total;
+  C.count = n;
+  C.next_id = h.nid;
+  C.hwm = n + 1;
+  C.nfree = 0;
+  C.bc_valid = h.bc_valid;
+  C.bc_tmin = h.tmin; C.bc_tmax = h.tmax;
+  C.bc_lo = h.lo32; C.bc_hi = h.hi32;
+  C.bc_elo = h.elo; C.bc_ehi = h.ehi;
+  __syncwarp();
+}
+
 __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint32_t k) {
   const uint32_t lane = lane_id();
   if (k >= out->count || C.count > out->stride) {

@@ -48,3 +48,7 @@ if os.environ.get("PHASES4"):
     t = ctr.astype(np.float64).sum(0)
     print("pass-2 scans: %.0f, entries/scan %.1f, cycles/scan %.0f, cycles per entry-per-lane %.1f"
           % (t[2], t[1] / t[2], t[0] / t[2], t[0] / (t[1] / 32)))
+if os.environ.get("LOADT"):
+    c = ctr.astype(np.float64)
+    print("snapshot load cycles per chain: median %.0f mean %.0f max %.0f; share of chain cycles %.3f"
+          % (np.median(c[:, 0]), c[:, 0].mean(), c[:, 0].max(), c[:, 0].sum() / cyc.sum()))
