@@ -52,3 +52,24 @@ if os.environ.get("LOADT"):
     c = ctr.astype(np.float64)
     print("snapshot load cycles per chain: median %.0f mean %.0f max %.0f; share of chain cycles %.3f"
           % (np.median(c[:, 0]), c[:, 0].mean(), c[:, 0].max(), c[:, 0].sum() / cyc.sum()))
+if os.environ.get("CHAINS"):
+    na, ns = len(w.alphas), len(g.segs)
+    cy = np.zeros(na * ns)
+    cy[g.chains.astype(np.int64)] = cyc[g.chains.astype(np.int64)] if cyc.shape[0] == na * ns else 0
+    M = cy.reshape(na, ns) / 1e6
+    print("per-alpha mean/max chain Mcycles:", [(a, round(M[i].mean(), 2), round(M[i].max(), 2)) for i, a in enumerate(w.alphas)])
+    segm = M.mean(0)
+    print("segment mean Mcycles: min %.2f median %.2f max %.2f" % (segm.min(), np.median(segm), segm.max()))
+    top = np.argsort(-cy)[:12]
+    print("top chains (alpha, seg, Mcyc, seg-mean):", [(w.alphas[c // ns], c % ns, round(cy[c] / 1e6, 2), round(segm[c % ns], 2)) for c in top])
+if os.environ.get("PHASES3A"):
+    na, ns = len(w.alphas), len(g.segs)
+    c = ctr.astype(np.uint64)
+    for ai, a in enumerate(w.alphas):
+        ids = [ai * ns + s for s in range(ns)]
+        sub = c[ids]
+        nreq = ns * w.window
+        sel, p2, rem = (sub[:, k].astype(np.float64).sum() / nreq / 1e3 for k in range(3))
+        p1 = float((sub[:, 3] >> np.uint64(32)).sum()) / nreq
+        fb = float((sub[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
+        print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f per req" % (a, sel, p2, rem, p1, fb))
