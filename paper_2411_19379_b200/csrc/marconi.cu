@@ -115,7 +115,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
 #endif
 #endif
       }
+#ifdef MC_CHAIN_SMID  // dev builds: SM id in the top 8 bits, cycles >> 10 below
+      if (P.chain_cycles) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        P.chain_cycles[c] = (sm << 24) | (uint32_t)min((long long)0xFFFFFF, (clock64() - t0) >> 10);
+      }
+#else
       if (P.chain_cycles) P.chain_cycles[c] = (uint32_t)min((long long)0xFFFFFFFF, (clock64() - t0) >> 10);
+#endif
     }
     __syncwarp();
   }
@@ -416,7 +424,10 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
                                                 kWarpsPerCta * 8ull * c->smem_nodes);
   c->blocks_per_sm = std::max(1, bps);
   c->ncap = max_nodes;
-  c->hcap = 2 * max_nodes;
+#ifndef MC_HASH_SHIFT
+#define MC_HASH_SHIFT 1
+#endif
+  c->hcap = max_nodes << MC_HASH_SHIFT;  // child-index entries (load factor <= 2^-MC_HASH_SHIFT)
   c->hv.assign(hv, hv + n_var);
   for (uint32_t v = 0; v < n_var; v++) {
     DevVariant d;

@@ -73,3 +73,7 @@ if os.environ.get("PHASES3A"):
         p1 = float((sub[:, 3] >> np.uint64(32)).sum()) / nreq
         fb = float((sub[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
         print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f per req" % (a, sel, p2, rem, p1, fb))
+if os.environ.get("DUMP"):
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.savez(os.environ["DUMP"], cycles=cyc, counters=ctr, chains=g.chains.astype(np.int64),
+             est=np.asarray(g.costs if hasattr(g, "costs") else [], np.int64))
