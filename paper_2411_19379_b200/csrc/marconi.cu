@@ -37,10 +37,10 @@ mc_status fail(mc_status s, const std::string& m) {
   } while (0)
 
 #ifndef MC_MINBLOCKS
-#define MC_MINBLOCKS 4
+#define MC_MINBLOCKS 16
 #endif
 #ifndef MC_WARPS_PER_CTA
-#define MC_WARPS_PER_CTA 4
+#define MC_WARPS_PER_CTA 1
 #endif
 constexpr int kWarpsPerCta = MC_WARPS_PER_CTA;
 }  // namespace

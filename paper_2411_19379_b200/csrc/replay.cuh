@@ -40,6 +40,11 @@ constexpr uint32_t D_PIN = 0x80000000u;    // on the current request's path (pin
 constexpr uint32_t D_MULTI = 0x40000000u;  // >= 2 children
 constexpr uint32_t D_FLAGS = D_PIN | D_MULTI;
 constexpr uint32_t T_MASK = 0x3FFFFFFFu;
+// Dense position = node slot.  A free slot (and slot 0, the root) holds a hole: both
+// flags set (never a candidate), t = T_MASK (never the t minimum) and e32 = NaN (fminf /
+// fmaxf ignore it); bound passes skip holes for the t maximum explicitly.
+constexpr uint32_t HOLE_TC = 0xFFFFFFFFu;
+constexpr uint32_t HOLE_E32 = 0x7FC00000u;
 constexpr uint32_t F_SSM = 1u;  // node flag (bits 24.. of NodeRec::nf)
 constexpr uint32_t NCH_MASK = 0x00FFFFFFu;
 // child-index entry (16 B): {first token, gen<<28 | parent slot<<14 | child slot,
@@ -89,8 +94,9 @@ struct DevSnapStore {
 // per snapshot at setup (image_kernel) so the 16+ chains that start from the same
 // snapshot copy it (coalesced, no child-index CAS, no Eq. 1 divisions) instead of
 // rebuilding it.  Byte layout from the image base (n = nodes):
-//   ImgHdr 64 | records 32(n+1) | ids 4(n+1) | dslot 4n | dense 8n | exact eff 8n |
+//   ImgHdr 64 | records 32(n+1) | ids 4(n+1) | dense 8(n+1) | exact eff 8(n+1) |
 //   child-index positions 4n | child-index entries 16n      (regions 16 B aligned)
+// (dense and eff are indexed by slot; slot 0, the root, is a hole)
 struct ImgHdr {
   unsigned long long total;
   uint32_t n, nid, tmin, tmax;
@@ -100,10 +106,9 @@ struct ImgHdr {
 };
 __host__ __device__ inline uint64_t img_al16(uint64_t x) { return (x + 15) & ~15ull; }
 __host__ __device__ inline uint64_t img_off_ids(uint32_t n) { return 64 + 32ull * (n + 1); }
-__host__ __device__ inline uint64_t img_off_dslot(uint32_t n) { return img_off_ids(n) + img_al16(4ull * (n + 1)); }
-__host__ __device__ inline uint64_t img_off_dense(uint32_t n) { return img_off_dslot(n) + img_al16(4ull * n); }
-__host__ __device__ inline uint64_t img_off_eff(uint32_t n) { return img_off_dense(n) + img_al16(8ull * n); }
-__host__ __device__ inline uint64_t img_off_tpos(uint32_t n) { return img_off_eff(n) + img_al16(8ull * n); }
+__host__ __device__ inline uint64_t img_off_dense(uint32_t n) { return img_off_ids(n) + img_al16(4ull * (n + 1)); }
+__host__ __device__ inline uint64_t img_off_eff(uint32_t n) { return img_off_dense(n) + img_al16(8ull * (n + 1)); }
+__host__ __device__ inline uint64_t img_off_tpos(uint32_t n) { return img_off_eff(n) + img_al16(8ull * (n + 1)); }
 __host__ __device__ inline uint64_t img_off_tent(uint32_t n) { return img_off_tpos(n) + img_al16(4ull * n); }
 __host__ __device__ inline uint64_t img_bytes(uint32_t n) { return img_off_tent(n) + 16ull * n; }
 // Writable view used by the live pass.
@@ -124,7 +129,7 @@ struct __align__(8) DenseRec {  // one dense position: the scanned key pair
 
 struct __align__(16) NodeRec {
   uint32_t parent, hidx, ds, de;  // hidx = position of the node's own entry in the child index
-  uint32_t roff, cxor, nf, dpos;  // roff = pool offset of the node's request; nf = nchild | flags << 24
+  uint32_t roff, cxor, nf, pad;   // roff = pool offset of the node's request; nf = nchild | flags << 24
 };
 
 struct KParams {
@@ -163,7 +168,7 @@ struct KParams {
 // Per-worker workspace slice.  The caller zero-initialises the workspace once
 // (header word 0 = child-index generation, word 1 = layout signature).
 // Slice layout (byte offsets from the slice base; n = ncap, h = hcap):
-//   header 256 | records 32n | ids 4n | dslot 4n | path 4n | freel 4n | child index 16h |
+//   header 256 | records 32n | ids 4n | scratch 4n | path 4n | freel 4n | child index 16h |
 //   dense tail 8n | exact eff (f64) 8n
 // (n is a power of two >= 64, so every region stays 16 B aligned).  ws_bytes_per_worker
 // is the end of the last region, so the accessors below and the stride cannot disagree.
@@ -181,7 +186,7 @@ struct WS {
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
   __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
-  __device__ __forceinline__ uint32_t* dslot() const { return (uint32_t*)(b + 256 + 36ull * n); }
+  __device__ __forceinline__ uint32_t* scratch() const { return (uint32_t*)(b + 256 + 36ull * n); }  // dump map
   __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n); }
   __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n); }
   __device__ __forceinline__ HEnt* tab() const { return (HEnt*)(b + ws_off_tab(n)); }
@@ -243,7 +248,7 @@ __device__ __forceinline__ double utility(Bounds b, uint32_t t, double e, double
 }
 struct Best {
   double u;
-  uint32_t t, id, i, slot;  // slot = dslot[i] when prefetched, else NIL
+  uint32_t t, id, i, slot;  // i = slot = the node's dense position
 };
 __device__ __forceinline__ bool better(double u, uint32_t t, uint32_t id, const Best& b) {
   return u < b.u || (u == b.u && (t < b.t || (t == b.t && id < b.id)));
@@ -277,7 +282,7 @@ struct Chain {
   DenseRec* sd;     // SMEM: dense {t_last|D_PIN|D_MULTI, RN32(eff)} for positions < S
   uint32_t S;       // SMEM-resident dense positions (the tail lives in global)
   uint32_t ncap, hmask, gen;
-  uint32_t count;     // live non-root nodes (= dense list length)
+  uint32_t count;     // live non-root nodes (the dense list spans slots [0, hwm), holes included)
   uint64_t total;     // bytes of all live nodes
   uint32_t next_id, hwm, nfree;
   DevModel m;
@@ -288,7 +293,6 @@ struct Chain {
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
-  uint32_t moved_slot, moved_pos;  // last eviction: node whose dense entry moved, and where
   // cached normalisation bounds (exact when bc_valid): adds extend them, removing or
   // changing a node that holds an extreme invalidates them (pass 1 then recomputes)
   // (bc_elo/bc_ehi: the exact fp64 extremes; bc_lo/bc_hi = their RN32 images, which are
@@ -311,8 +315,6 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.nfree = __shfl_sync(FULL, C.nfree, 0);
   C.c_wr = __shfl_sync(FULL, (unsigned long long)C.c_wr, 0);
   C.failed = __shfl_sync(FULL, (int)C.failed, 0);
-  C.moved_slot = __shfl_sync(FULL, C.moved_slot, 0);
-  C.moved_pos = __shfl_sync(FULL, C.moved_pos, 0);
   C.bc_valid = __shfl_sync(FULL, C.bc_valid, 0);
   C.bc_tmin = __shfl_sync(FULL, C.bc_tmin, 0);
   C.bc_tmax = __shfl_sync(FULL, C.bc_tmax, 0);
@@ -424,10 +426,13 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
 __device__ __forceinline__ DenseRec* d_ptr(const Chain& C, uint32_t i) { return i < C.S ? C.sd + i : C.w.tail() + i; }
 __device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return d_ptr(C, i)->tc; }
 __device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return C.w.eff64()[i]; }
-// dense position -> slot (global: shared memory is reserved for the scanned dense words)
-__device__ __forceinline__ uint32_t d_slot(const Chain& C, uint32_t i) { return C.w.dslot()[i]; }
-__device__ __forceinline__ void d_set_slot(Chain& C, uint32_t i, uint32_t s) { C.w.dslot()[i] = s; }
-__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[d_slot(C, i)]; }
+__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[i]; }
+__device__ __forceinline__ void d_hole(Chain& C, uint32_t i) {
+  DenseRec h;
+  h.tc = HOLE_TC;
+  h.e32 = __uint_as_float(HOLE_E32);
+  *d_ptr(C, i) = h;
+}
 __device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
 // bound-cache hooks (lane 0, or uniform)
 __device__ __forceinline__ void bc_extend_e(Chain& C, float e32, double e64) {
@@ -469,10 +474,9 @@ __device__ __forceinline__ void d_multi(Chain& C, uint32_t i, uint32_t nchild) {
   d->tc = (d->tc & ~D_MULTI) | (nchild >= C.mthr ? D_MULTI : 0u);
 }
 __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
-  const uint32_t i = C.count++;
-  NodeRec& R = C.w.rec()[s];
-  R.dpos = i;
-  d_set_slot(C, i, s);
+  const uint32_t i = s;
+  C.count++;
+  const NodeRec& R = C.w.rec()[s];
   const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
   C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
@@ -555,8 +559,9 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   __syncwarp();
   if (lane == 0) {
     NodeRec z;
-    z.parent = NIL; z.hidx = NIL; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.dpos = NIL;
+    z.parent = NIL; z.hidx = NIL; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.pad = 0;
     C.w.rec()[0] = z;
+    d_hole(C, 0);  // the root is never a candidate and not in the bounds
   }
   uint64_t bytes = 0;
   bool bad = false;
@@ -574,10 +579,9 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     R.roff = (uint32_t)r.ref_off;
     R.cxor = 0;
     R.nf = (r.has_ssm ? F_SSM : 0u) << 24;
-    R.dpos = i;
+    R.pad = 0;
     C.w.rec()[s] = R;
     C.w.ids()[s] = r.id;
-    d_set_slot(C, i, s);
     bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
@@ -608,8 +612,8 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
     const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
-    C.w.eff64()[i] = v;
-    DenseRec* d = d_ptr(C, i);
+    C.w.eff64()[s] = v;
+    DenseRec* d = d_ptr(C, s);
     d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
     // vLLM+ keeps the node id in the second dense word (LRU key (t, id)); Marconi RN32(eff)
     d->e32 = C.block ? __uint_as_float(nodes[i].id) : __double2float_rn(v);
@@ -644,7 +648,7 @@ __device__ void export_image(Chain& C, char* dst) {
   double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
   const DenseRec* dense = C.w.tail();
   const double* e64 = C.w.eff64();
-  for (uint32_t i = lane; i < n; i += 32) {
+  for (uint32_t i = lane + 1; i <= n; i += 32) {  // slots 1..n (slot 0 = root hole)
     const DenseRec d = dense[i];
     const uint32_t t = d.tc & T_MASK;
     tmn = min(tmn, t);
@@ -665,20 +669,16 @@ __device__ void export_image(Chain& C, char* dst) {
     elo = a < elo ? a : elo;
     ehi = b > ehi ? b : ehi;
   }
-  // records, ids, dslot, dense, eff
+  // records, ids, dense, eff (all by slot)
   NodeRec* rec = (NodeRec*)(dst + 64);
   uint32_t* ids = (uint32_t*)(dst + img_off_ids(n));
-  uint32_t* dsl = (uint32_t*)(dst + img_off_dslot(n));
   DenseRec* dn = (DenseRec*)(dst + img_off_dense(n));
   double* ef = (double*)(dst + img_off_eff(n));
   for (uint32_t i = lane; i <= n; i += 32) {
     rec[i] = C.w.rec()[i];
     ids[i] = C.w.ids()[i];
-  }
-  for (uint32_t i = lane; i < n; i += 32) {
-    dsl[i] = C.w.dslot()[i];
     dn[i] = dense[i];
-    ef[i] = e64[i];
+    ef[i] = (i == 0) ? 0.0 : e64[i];
   }
   // occupied child-index slots of this generation, compacted in slot order
   uint32_t* tpos = (uint32_t*)(dst + img_off_tpos(n));
@@ -738,25 +738,25 @@ __device__ __forceinline__ void warp_copy16(uint4* __restrict__ d, const uint4* 
 __device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S, const char* __restrict__ src,
                                         uint32_t n, uint32_t g) {
   const uint32_t lane = lane_id();
-  // records + ids + dslot are contiguous in the image but not in the slice
+  // records + ids are contiguous in the image but not in the slice
   warp_copy16((uint4*)w.rec(), (const uint4*)(src + 64), 2 * (n + 1));
   warp_copy16((uint4*)w.ids(), (const uint4*)(src + img_off_ids(n)), (uint32_t)(img_al16(4ull * (n + 1)) / 16));
-  warp_copy16((uint4*)w.dslot(), (const uint4*)(src + img_off_dslot(n)), (uint32_t)(img_al16(4ull * n) / 16));
-  warp_copy16((uint4*)w.eff64(), (const uint4*)(src + img_off_eff(n)), (n + 1) / 2);
+  warp_copy16((uint4*)w.eff64(), (const uint4*)(src + img_off_eff(n)), (n + 2) / 2);
   {
-    const uint32_t ns = min(n, S);
+    const uint32_t m = n + 1;  // slots 0..n
+    const uint32_t ns = min(m, S);
     const DenseRec* dn = (const DenseRec*)(src + img_off_dense(n));
-    for (uint32_t b = 0; b < n; b += 32 * kCopyU) {  // SMEM part and global tail
+    for (uint32_t b = 0; b < m; b += 32 * kCopyU) {  // SMEM part and global tail
       DenseRec v[kCopyU];
 #pragma unroll
       for (int q = 0; q < kCopyU; q++) {
         const uint32_t i = b + 32 * q + lane;
-        if (i < n) v[q] = dn[i];
+        if (i < m) v[q] = dn[i];
       }
 #pragma unroll
       for (int q = 0; q < kCopyU; q++) {
         const uint32_t i = b + 32 * q + lane;
-        if (i < n) *(i < ns ? sd + i : w.tail() + i) = v[q];
+        if (i < m) *(i < ns ? sd + i : w.tail() + i) = v[q];
       }
     }
   }
@@ -834,8 +834,20 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
   }
   mc_snap_node* dst = out->nodes + (uint64_t)k * out->stride;
   uint32_t* pdst = out->pidx + (uint64_t)k * out->stride;
-  for (uint32_t i = lane; i < C.count; i += 32) {
-    const uint32_t s = d_slot(C, i);
+  // output index of every live slot (slot order), kept in the scratch map
+  uint32_t* map = C.w.scratch();
+  uint32_t w = 0;
+  for (uint32_t b = 0; b < C.hwm; b += 32) {
+    const uint32_t s = b + lane;
+    const bool live = s < C.hwm && d_tc(C, s) != HOLE_TC;
+    const unsigned bl = __ballot_sync(FULL, live);
+    if (live) map[s] = w + __popc(bl & ((1u << lane) - 1u));
+    w += __popc(bl);
+  }
+  __syncwarp();
+  for (uint32_t s = lane; s < C.hwm; s += 32) {
+    if (d_tc(C, s) == HOLE_TC) continue;
+    const uint32_t i = map[s];
     const NodeRec R = C.w.rec()[s];
     const uint32_t p = R.parent;
     mc_snap_node r;
@@ -844,10 +856,10 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
     r.ref_off = R.roff;
     r.d_start = R.ds;
     r.d_end = R.de;
-    r.t_last = d_tc(C, i) & T_MASK;
+    r.t_last = d_tc(C, s) & T_MASK;
     r.has_ssm = ((R.nf >> 24) & F_SSM) ? 1u : 0u;
     dst[i] = r;
-    pdst[i] = (p == 0) ? NIL : C.w.rec()[p].dpos;
+    pdst[i] = (p == 0) ? NIL : map[p];
   }
   if (lane == 0) {
     out->off[k] = (uint64_t)k * out->stride;
@@ -941,8 +953,7 @@ __device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const Dense
   return make_double2(elo, ehi);
 }
 __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* tail, const double* e64,
-                                          const uint32_t* dslot, const uint32_t* ids, uint32_t cnt, uint32_t S,
-                                          Bounds b, double alpha) {
+                                          const uint32_t* ids, uint32_t cnt, uint32_t S, Bounds b, double alpha) {
   const uint32_t lane = lane_id();
   Best best;
   best_init(best);
@@ -950,7 +961,7 @@ __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* ta
     const uint32_t tc = (i < S ? sd[i] : tail[i]).tc;
     if (tc & D_FLAGS) continue;
     const double u = utility(b, tc, e64[i], alpha);
-    const uint32_t id = ids[dslot[i]];
+    const uint32_t id = ids[i];
     if (best.i == NIL || better(u, tc, id, best)) {
       best.u = u; best.t = tc; best.id = id; best.i = i;
     }
@@ -967,7 +978,7 @@ __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* ta
 //          pass 2 reads only those fp64 values).  Pass 2 -- fp32 filter key per candidate,
 //          best two per lane.  Verify -- exact IEEE utility of the entries within δ of
 //          the minimum key; near-ties -> exact full pass.
-__device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b) {
+__device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Bounds& b, bool need_u) {
   const uint32_t lane = lane_id();
   Best best;
   best_init(best);
@@ -976,7 +987,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     scan_dense(C, cnt, [&](int, uint32_t i, uint32_t tc, float) {
       const uint32_t t = tc & T_MASK;
       b.tmin = min(b.tmin, t);
-      b.tmax = max(b.tmax, t);
+      b.tmax = max(b.tmax, tc == HOLE_TC ? 0u : t);
       if (!(tc & D_FLAGS) && t <= best.t) {
         if (t < best.t) {
           best.t = t; best.i = i; best.id = NIL;  // id fetched lazily on a t tie
@@ -987,7 +998,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
         }
       }
     });
-    if (best.i != NIL) best.slot = d_slot(C, best.i);  // for the removal
+    best.slot = best.i;  // for the removal
     // resolve ids only when lanes tie on the minimum t
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -1041,7 +1052,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   scan_dense(C, cnt, [&](int q, uint32_t, uint32_t tc, float e) {
     const uint32_t t = tc & T_MASK;
     tmn[q] = min(tmn[q], t);
-    tmx[q] = max(tmx[q], t);
+    tmx[q] = max(tmx[q], tc == HOLE_TC ? 0u : t);
     lo[q] = fminf(lo[q], e);
     hi[q] = fmaxf(hi[q], e);
   });
@@ -1106,10 +1117,6 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     if (a1[q] < k1) { k2 = fminf(k1, a2[q]); k1 = a1[q]; i1 = ai[q]; }
     else { k2 = fminf(k2, a1[q]); }
   }
-  // issue the fp64 reads this lane may need (extremes, its best candidate) before the
-  // warp reductions so their latency overlaps the shuffles
-  const double pre_k1 = (i1 != NIL) ? e64[i1] : 0.0;
-  const uint32_t pre_slot = (i1 != NIL) ? d_slot(C, i1) : NIL;
   float kmin = k1;
 #pragma unroll
   for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
@@ -1122,26 +1129,25 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   const double lim = (double)kmin + delta;
   if (!exact_only && !__any_sync(FULL, (double)k2 <= lim)) {
     const bool mine = (double)k1 <= lim;
-    if (mine) {
-#ifdef MC_PREFETCH_VICTIM
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(C.w.rec() + pre_slot));  // the removal reads it next
-#endif
-      best.t = d_tc(C, i1);
-      best.u = utility(b, best.t, pre_k1, C.alpha);
-      best.i = i1;
-      best.slot = pre_slot;
-    }
     const unsigned who = __ballot_sync(FULL, mine);
     if (__popc(who) == 1) {  // the common case: one candidate survives the filter
       const int src = __ffs(who) - 1;
-      best.u = __shfl_sync(FULL, best.u, src);
-      best.t = __shfl_sync(FULL, best.t, src);
-      best.i = __shfl_sync(FULL, best.i, src);
-      best.slot = __shfl_sync(FULL, best.slot, src);
+      best.i = __shfl_sync(FULL, i1, src);
+      best.slot = best.i;
       best.id = NIL;
+      if (need_u) {  // the exact utility is only logged (no global read otherwise)
+        if (mine) best.u = utility(b, d_tc(C, i1), e64[i1], C.alpha);
+        best.u = __shfl_sync(FULL, best.u, src);
+      }
       return best;
     }
-    if (mine) best.id = d_id(C, i1);  // ids only matter for exact ties
+    if (mine) {  // near-ties: exact utilities, ids for exact ties
+      best.t = d_tc(C, i1);
+      best.u = utility(b, best.t, e64[i1], C.alpha);
+      best.i = i1;
+      best.slot = i1;
+      best.id = d_id(C, i1);
+    }
     best_reduce(best);
     return best;
   }
@@ -1149,7 +1155,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   CC.t_unpin += 1;  // number of exact fallback passes
 #endif
   // near-ties / unresolvable fp32 range: exact full pass (cold path)
-  return exact_select(C.sd, C.w.tail(), e64, C.w.dslot(), C.w.ids(), cnt, C.S, b, C.alpha);
+  return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.alpha);
 }
 
 __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
@@ -1159,7 +1165,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
 #ifdef MC_PHASE_TIMERS3
   long long _e3 = clock64();
 #endif
-  const Best best = select_victim(C, cnt, b);
+  const Best best = select_victim(C, C.hwm, b, log != nullptr);
 #ifdef MC_PHASE_TIMERS3
   { long long _n = clock64(); C.t_walk += (unsigned long long)(_n - _e3); _e3 = _n; }
 #endif
@@ -1173,17 +1179,14 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
   if (lane == 0) {
     // Loads first (independent ones back to back), then the stores: every store
     // below targets fields no later load in this block reads.
-    const uint32_t last = cnt - 1;
-    const uint32_t sl = d_slot(C, last);        // node moved into the freed dense position
-    const double e_last = C.w.eff64()[last];
-    const uint32_t x = (best.slot != NIL) ? best.slot : d_slot(C, best.i);
+    const uint32_t x = best.i;  // slot = dense position
     const NodeRec X = C.w.rec()[x];
     const uint32_t p = X.parent;
     const uint32_t xf = X.nf >> 24;
     const NodeRec Rp = C.w.rec()[p];
     const uint32_t xid = log ? C.w.ids()[x] : 0u;
+    const DenseRec dv = *d_ptr(C, x);
     uint32_t kind;
-    double e_moved = e_last;
     if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
       kind = 0;
       C.total -= node_bytes(C.m, X.ds, X.de, xf & F_SSM);
@@ -1191,7 +1194,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       NodeRec& Wp = C.w.rec()[p];
       Wp.nf = Rp.nf - 1;
       Wp.cxor = Rp.cxor ^ x;
-      if (p != 0) d_multi(C, Rp.dpos, (Rp.nf & NCH_MASK) - 1);
+      if (p != 0) d_multi(C, p, (Rp.nf & NCH_MASK) - 1);
       C.c_wr += 1;
     } else {  // one child: release the state, the child absorbs the KVs
       kind = 1;
@@ -1209,8 +1212,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       hash_erase_at_1(C, hc);
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
       const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
-      d_set_eff(C, Rc.dpos, ec);
-      if (Rc.dpos == last) e_moved = ec;
+      d_set_eff(C, c, ec);
       C.c_wr += 2;
     }
     if (log) {
@@ -1222,22 +1224,10 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       }
       *log_n = li + 1;
     }
-    // dense_remove: move the last dense entry into the victim's position
-    const uint32_t i = X.dpos;
-    {
-      const DenseRec dv = *d_ptr(C, i);
-      bc_remove(C, dv.tc & T_MASK, dv.e32);
-    }
-    C.moved_slot = NIL;
-    if (i != last) {
-      C.moved_slot = sl;
-      C.moved_pos = i;
-      *d_ptr(C, i) = *d_ptr(C, last);
-      C.w.eff64()[i] = e_moved;
-      d_set_slot(C, i, sl);
-      C.w.rec()[sl].dpos = i;
-    }
-    C.count = last;
+    // the victim's slot becomes a hole (no dense entry moves)
+    bc_remove(C, dv.tc & T_MASK, dv.e32);
+    d_hole(C, x);
+    C.count = cnt - 1;
     C.w.rec()[x].nf = 0;
     C.w.freel()[C.nfree++] = x;
   }
@@ -1260,7 +1250,7 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   const uint32_t ytok = C.w.tab()[hi].tok;
   NodeRec U;
   U.parent = Y.parent; U.hidx = hi; U.ds = Y.ds; U.de = x;
-  U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.dpos = NIL;
+  U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.pad = 0;
   C.w.rec()[u] = U;
   C.w.ids()[u] = C.next_id++;
   C.w.tab()[hi] = hmake(C, Y.parent, ytok, u, x, stateful, Y.roff);  // same key, new child
@@ -1270,14 +1260,14 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   Ry.hidx = hash_insert_1(C, hmake(C, u, ft, y, Y.de, (Y.nf >> 24) & F_SSM, Y.roff), u);
   C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
-  d_set_eff(C, Y.dpos, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
+  d_set_eff(C, y, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
   C.c_wr += 2;
   return u;
 }
 
 __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   NodeRec& R = C.w.rec()[x];
-  const uint32_t nf = R.nf, dp = R.dpos, ds = R.ds, de = R.de, hi = R.hidx;
+  const uint32_t nf = R.nf, dp = x, ds = R.ds, de = R.de, hi = R.hidx;
   R.nf = nf | (F_SSM << 24);
   C.w.tab()[hi].de = de | 0x80000000u;  // the child index carries the state flag for the walk
   d_set_eff(C, dp, node_eff(C.m, ds, de, true));
@@ -1348,7 +1338,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     if (lane == 0 && npath >= 32) C.w.path()[npath] = c;
     if (lane == npath) {
       my_path = c; my_ds = pos; my_de = de; my_fl = fl;
-      my_dp = C.w.rec()[c].dpos;  // for the pin step; the load overlaps the rest of the walk
+      my_dp = c;  // dense position = slot
     }
     npath++;
     pinned_bytes += node_bytes(C.m, pos, de, fl & F_SSM);
@@ -1399,7 +1389,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   }
   if (lane == 0)
     for (uint32_t i = 32; i < npath; i++) {
-      DenseRec* d = d_ptr(C, C.w.rec()[C.w.path()[i]].dpos);
+      DenseRec* d = d_ptr(C, C.w.path()[i]);
       if (i == hit_idx) old_t = d->tc & T_MASK;
       d->tc = (i == hit_idx ? (r | (d->tc & D_MULTI)) : d->tc) | D_PIN;
     }
@@ -1483,7 +1473,6 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     // Step 7: evict the argmin utility until the request fits.
     while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + d_nodes > C.capn))) {
       evict_one(C, P, r, log, log_n);
-      if (my_path == C.moved_slot && C.moved_slot != NIL) my_dp = C.moved_pos;  // keep the pin target current
     }
     PHASE_MARK(C.t_evict);
     // Step 8: insert.
@@ -1513,20 +1502,20 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
           const NodeRec Ra = C.w.rec()[attach];
           NodeRec W;
           W.parent = attach; W.hidx = NIL; W.ds = m; W.de = n;
-          W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.dpos = NIL;
+          W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.pad = 0;
           C.w.rec()[w] = W;
           C.w.ids()[w] = C.next_id++;
           C.w.rec()[w].hidx = hash_insert_1(C, hmake(C, attach, ft, w, n, true, (uint32_t)off), attach);
           NodeRec& Wa = C.w.rec()[attach];
           Wa.nf = Ra.nf + 1;
           Wa.cxor = Ra.cxor ^ w;
-          if (attach != 0) d_multi(C, Ra.dpos, (Ra.nf & NCH_MASK) + 1);
+          if (attach != 0) d_multi(C, attach, (Ra.nf & NCH_MASK) + 1);
           dense_add_1(C, w, r);
           C.c_wr += 1;
         }
       } else if (partial == NIL) {
         // final node at n already exists: timestamp it (R5)
-        d_stamp(C, C.w.rec()[v].dpos, r);
+        d_stamp(C, v, r);
         if (n_gain == NIL && p_gain != v) C.c_wr += 1;
       }
       C.total += d_bytes;
@@ -1545,7 +1534,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   }
   if (lane == 0) {
     for (uint32_t i = 32; i < npath; i++) {
-      DenseRec* d = d_ptr(C, C.w.rec()[C.w.path()[i]].dpos);
+      DenseRec* d = d_ptr(C, C.w.path()[i]);
       d->tc &= ~D_PIN;
     }
     if (reuse > L_in) {
@@ -1623,8 +1612,8 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
     for (int q = 0; q < K; q++) { key[q] = INF64; pos[q] = NIL; }
     uint64_t wl = INF64;
     uint32_t tmax = 0;
-    scan_dense(C, C.count, [&](int, uint32_t i, uint32_t tc, float e) {
-      tmax = max(tmax, tc & T_MASK);
+    scan_dense(C, C.hwm, [&](int, uint32_t i, uint32_t tc, float e) {
+      tmax = max(tmax, tc == HOLE_TC ? 0u : (tc & T_MASK));
       if (tc & D_FLAGS) return;
       const uint64_t k = ((uint64_t)(tc & T_MASK) << 32) | __float_as_uint(e);
       if (k < key[K - 1]) {
@@ -1667,8 +1656,7 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
       uint32_t e_pos = NIL;
       uint64_t e_key = INF64;
       if (lane == 0) {
-        const uint32_t x = d_slot(C, vpos);
-        const uint32_t sl = d_slot(C, last);
+        const uint32_t x = vpos;  // slot = dense position
         const NodeRec X = C.w.rec()[x];
         const uint32_t p = X.parent;
         const NodeRec Rp = C.w.rec()[p];
@@ -1677,7 +1665,7 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
         NodeRec& Wp = C.w.rec()[p];
         Wp.nf = Rp.nf - 1;
         Wp.cxor = Rp.cxor ^ x;
-        if (p != 0) d_multi(C, Rp.dpos, (Rp.nf & NCH_MASK) - 1);
+        if (p != 0) d_multi(C, p, (Rp.nf & NCH_MASK) - 1);
         if (log) {
           const uint32_t li = *log_n;
           if (li < P.log_cap) {
@@ -1688,17 +1676,13 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
           }
           *log_n = li + 1;
         }
-        if (vpos != last) {
-          *d_ptr(C, vpos) = *d_ptr(C, last);
-          d_set_slot(C, vpos, sl);
-          C.w.rec()[sl].dpos = vpos;
-        }
+        d_hole(C, vpos);
         C.count = last;
         C.w.rec()[x].nf = 0;
         C.w.freel()[C.nfree++] = x;
         C.c_wr += 1;
         if (p != 0 && (Rp.nf & NCH_MASK) == 1) {  // the parent lost its last child
-          const uint32_t pp = (Rp.dpos == last) ? vpos : Rp.dpos;
+          const uint32_t pp = p;
           const DenseRec dp = *d_ptr(C, pp);
           if (!(dp.tc & D_FLAGS)) {
             e_pos = pp;
@@ -1711,10 +1695,6 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
       C.n_evict++;
       need--;
       progressed = true;
-      // the entry that moved from `last` into the victim's position keeps its listing
-#pragma unroll
-      for (int q = 0; q < K; q++)
-        if (pos[q] == last) pos[q] = vpos;
       e_pos = __shfl_sync(FULL, e_pos, 0);
       e_key = __shfl_sync(FULL, (unsigned long long)e_key, 0);
       if (e_pos != NIL && e_key < W) {  // keep the exposed parent (else W covers it)
@@ -1788,14 +1768,13 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
 #ifdef MC_DEBUG
   for (uint32_t i = lane; i < mb; i += 32) {
     const uint32_t sl = path[i];
-    if (sl >= C.hwm || C.w.rec()[sl].dpos >= C.count)
-      printf("vllm walk: r %u k %u/%u slot %u hwm %u dpos %u count %u nb %u S %u\n", r, i, mb, sl, C.hwm,
-             sl < C.ncap ? C.w.rec()[sl].dpos : 0u, C.count, nb, C.S);
+    if (sl >= C.hwm || d_tc(C, sl) == HOLE_TC)
+      printf("vllm walk: r %u k %u/%u slot %u hwm %u count %u nb %u S %u\n", r, i, mb, sl, C.hwm, C.count, nb, C.S);
   }
 #endif
   // Step 3: touch (t_last = r) and pin every matched block (V5, V7), in parallel.
   for (uint32_t i = lane; i < mb; i += 32) {
-    DenseRec* d = d_ptr(C, C.w.rec()[path[i]].dpos);
+    DenseRec* d = d_ptr(C, path[i]);
     d->tc = r | (d->tc & D_MULTI) | D_PIN;
   }
   C.c_wr += mb;
@@ -1836,7 +1815,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           R.roff = (uint32_t)off;
           R.cxor = inner ? path[k + 1] : 0u;
           R.nf = (F_SSM << 24) | (inner ? 1u : 0u);
-          R.dpos = cnt0 + j;
+          R.pad = 0;
           const uint32_t h = block_hash_1(P.tok + off + (uint64_t)k * x, x);
           uint32_t hi = hslot(par, h, C.hmask);
           const uint32_t nk = hkey(C, par, s);
@@ -1852,8 +1831,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           R.hidx = hi;
           C.w.rec()[s] = R;
           C.w.ids()[s] = id0 + j;
-          d_set_slot(C, cnt0 + j, s);
-          DenseRec* d = d_ptr(C, cnt0 + j);
+          DenseRec* d = d_ptr(C, s);
           d->tc = r | (inner ? D_MULTI : 0u);
           d->e32 = __uint_as_float(id0 + j);  // vLLM+: the id, so (t, id) LRU keys need no global read
         }
@@ -1863,7 +1841,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           Rv.nf = nf0 + 1;
           Rv.cxor ^= path[mb];
           if (v != 0 && (nf0 & NCH_MASK) + 1 >= C.mthr) {
-            DenseRec* d = d_ptr(C, Rv.dpos);
+            DenseRec* d = d_ptr(C, v);
             d->tc |= D_MULTI;
           }
           C.nfree -= take;
@@ -1883,7 +1861,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   }
   // Unpin the matched path (evictions may have moved dense entries: positions re-read).
   for (uint32_t i = lane; i < mb; i += 32) {
-    DenseRec* d = d_ptr(C, C.w.rec()[path[i]].dpos);
+    DenseRec* d = d_ptr(C, path[i]);
     d->tc &= ~D_PIN;
   }
   __syncwarp();
@@ -1913,8 +1891,6 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.alpha = V.block ? 0.0 : alpha;  // vLLM+ is LRU: α does not apply
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;
-  C.moved_slot = NIL;
-  C.moved_pos = 0;
   C.bc_valid = 0;
   C.bc_tmin = 0; C.bc_tmax = 0; C.bc_lo = 0.0f; C.bc_hi = 0.0f; C.bc_elo = 0.0; C.bc_ehi = 0.0;
 #if defined(MC_PHASE_TIMERS) || defined(MC_PHASE_TIMERS3)
