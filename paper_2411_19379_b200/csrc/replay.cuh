@@ -895,7 +895,7 @@ __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, 
 }
 
 #ifndef MC_UNROLL
-#define MC_UNROLL 2
+#define MC_UNROLL 4
 #endif
 constexpr int kUnroll = MC_UNROLL;
 
