@@ -293,7 +293,9 @@ struct Chain {
   double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
-  // cached normalisation bounds (exact when bc_valid): adds extend them, removing or
+  // cached normalisation bounds (bc_valid bit 0: t and fp32 eff bounds exact; bits 1 / 2:
+  // bc_elo / bc_ehi also exact -- recovered lazily, only a logged or near-tied victim
+  // needs them): adds extend them, removing or
   // changing a node that holds an extreme invalidates them (pass 1 then recomputes)
   // (bc_elo/bc_ehi: the exact fp64 extremes; bc_lo/bc_hi = their RN32 images, which are
   // the fp32 extremes because RN is monotone)
@@ -435,9 +437,13 @@ __device__ __forceinline__ void d_hole(Chain& C, uint32_t i) {
 }
 __device__ __forceinline__ void d_set_tc(Chain& C, uint32_t i, uint32_t v) { d_ptr(C, i)->tc = v; }
 // bound-cache hooks (lane 0, or uniform)
+// RN32 is monotone, so e32 < lo32 implies e64 is below every live value: the new exact
+// minimum is known even when the old one was not (likewise for the maximum).
 __device__ __forceinline__ void bc_extend_e(Chain& C, float e32, double e64) {
-  if (e64 < C.bc_elo) { C.bc_elo = e64; C.bc_lo = e32; }
-  if (e64 > C.bc_ehi) { C.bc_ehi = e64; C.bc_hi = e32; }
+  if (e32 < C.bc_lo) { C.bc_lo = e32; C.bc_elo = e64; C.bc_valid |= 2u; }
+  else if (e32 == C.bc_lo && e64 < C.bc_elo) C.bc_elo = e64;
+  if (e32 > C.bc_hi) { C.bc_hi = e32; C.bc_ehi = e64; C.bc_valid |= 4u; }
+  else if (e32 == C.bc_hi && e64 > C.bc_ehi) C.bc_ehi = e64;
 }
 __device__ __forceinline__ void bc_add(Chain& C, uint32_t t, float e32, double e64) {
   C.bc_tmin = min(C.bc_tmin, t);
@@ -818,7 +824,7 @@ __device__ void load_image(Chain& C, const KParams& P, const char* src) {
   C.next_id = h.nid;
   C.hwm = n + 1;
   C.nfree = 0;
-  C.bc_valid = h.bc_valid;
+  C.bc_valid = h.bc_valid ? 7u : 0u;  // the image carries exact fp64 extremes
   C.bc_tmin = h.tmin; C.bc_tmax = h.tmax;
   C.bc_lo = h.lo32; C.bc_hi = h.hi32;
   C.bc_elo = h.elo; C.bc_ehi = h.ehi;
@@ -950,6 +956,12 @@ __device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const Dense
     if (e == lo32) elo = fmin(elo, e64[i]);
     if (e == hi32) ehi = fmax(ehi, e64[i]);
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double xl = __shfl_xor_sync(FULL, elo, o), xh = __shfl_xor_sync(FULL, ehi, o);
+    elo = xl < elo ? xl : elo;
+    ehi = xh > ehi ? xh : ehi;
+  }
   return make_double2(elo, ehi);
 }
 __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* tail, const double* e64,
@@ -1039,9 +1051,9 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   // the cached bounds are known exact
   uint32_t tmin, tmax;
   float lo32, hi32;
-  if (C.bc_valid) {
+  Chain& Cw = const_cast<Chain&>(C);
+  if (C.bc_valid & 1u) {
     tmin = C.bc_tmin; tmax = C.bc_tmax; lo32 = C.bc_lo; hi32 = C.bc_hi;
-    b.emin = C.bc_elo; b.emax = C.bc_ehi;
   } else {
   uint32_t tmn[kUnroll], tmx[kUnroll];
   float lo[kUnroll], hi[kUnroll];
@@ -1069,19 +1081,8 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     lo32 = fminf(lo32, __shfl_xor_sync(FULL, lo32, o));
     hi32 = fmaxf(hi32, __shfl_xor_sync(FULL, hi32, o));
   }
-  // exact fp64 extremes: the fp64 values of the entries holding the fp32 extremes
-  double2 ex = recover_extremes(C.sd, C.w.tail(), C.w.eff64(), cnt, C.S, lo32, hi32);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const double xl = __shfl_xor_sync(FULL, ex.x, o), xh = __shfl_xor_sync(FULL, ex.y, o);
-    ex.x = xl < ex.x ? xl : ex.x;
-    ex.y = xh > ex.y ? xh : ex.y;
-  }
-  b.emin = ex.x;
-  b.emax = ex.y;
-  Chain& Cw = const_cast<Chain&>(C);
+  // the exact fp64 extremes are recovered only when a victim's exact utility is needed
   Cw.bc_valid = 1; Cw.bc_tmin = tmin; Cw.bc_tmax = tmax; Cw.bc_lo = lo32; Cw.bc_hi = hi32;
-  Cw.bc_elo = ex.x; Cw.bc_ehi = ex.y;
 #ifdef MC_PHASE_TIMERS3
   CC.t_unpin += 1ull << 32;  // count full bound passes (high half)
 #endif
@@ -1122,7 +1123,17 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
   T3(t_evict);
   if (kmin == INF) return best;  // no candidate
+  // exact fp64 extremes (lazily, the fp64 values of the entries holding the fp32 extremes)
+#define ENSURE_EXTREMES()                                                                  \
+  do {                                                                                     \
+    if ((C.bc_valid & 6u) != 6u) {                                                         \
+      const double2 ex = recover_extremes(C.sd, C.w.tail(), e64, cnt, C.S, lo32, hi32);    \
+      Cw.bc_elo = ex.x; Cw.bc_ehi = ex.y; Cw.bc_valid |= 6u;                               \
+    }                                                                                      \
+    b.emin = C.bc_elo; b.emax = C.bc_ehi;                                                  \
+  } while (0)
   // δ = 2^-19 (1 + α (1 + 4 emax/Δe32)); a zero fp32 range cannot resolve eff -> exact pass
+  if (de32 == 0.0) ENSURE_EXTREMES();
   const bool exact_only = (de32 == 0.0) && (b.emax != b.emin);
   const double ratio = (de32 == 0.0) ? 0.0 : __ddiv_rn((double)hi32, de32);
   const double delta = 1.9073486328125e-06 * (1.0 + C.alpha * (1.0 + 4.0 * ratio));
@@ -1136,11 +1147,13 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.slot = best.i;
       best.id = NIL;
       if (need_u) {  // the exact utility is only logged (no global read otherwise)
+        ENSURE_EXTREMES();
         if (mine) best.u = utility(b, d_tc(C, i1), e64[i1], C.alpha);
         best.u = __shfl_sync(FULL, best.u, src);
       }
       return best;
     }
+    ENSURE_EXTREMES();
     if (mine) {  // near-ties: exact utilities, ids for exact ties
       best.t = d_tc(C, i1);
       best.u = utility(b, best.t, e64[i1], C.alpha);
@@ -1155,6 +1168,8 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   CC.t_unpin += 1;  // number of exact fallback passes
 #endif
   // near-ties / unresolvable fp32 range: exact full pass (cold path)
+  ENSURE_EXTREMES();
+#undef ENSURE_EXTREMES
   return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.alpha);
 }
 

@@ -4,6 +4,5 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 tail -15 gpurun_out/pytest_gpu.log
 run() { f=$1; shift; echo "== $f $*"; env "$@" MARCONI_LIB=$PWD/build/variants/$f CFG=${CFG:-3} timeout 300 python tools/variant_timing.py 2>&1 | tail -3; }
 for i in 1 2; do
-run w1.so A=1
-run slot.so A=1
+for f in build/variants/*.so; do run $(basename $f) A=1; done
 done
