@@ -51,7 +51,11 @@ constexpr int kWarpsPerCta = MC_WARPS_PER_CTA;
 // kPolicy 0 = Marconi chains, 1 = vLLM+ chains (block_size > 0): one instantiation per
 // policy so the Marconi kernel carries no vLLM+ code (registers, instruction cache).
 template <int kPolicy>
+#ifdef MC_MAXNREG  // explicit register budget (sizes the resident warps per SM instead of MC_MINBLOCKS)
+__global__ void __maxnreg__(MC_MAXNREG) replay_kernel(KParams P) {
+#else
 __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel(KParams P) {
+#endif
   extern __shared__ __align__(16) char smem[];
   const uint32_t lane = lane_id();
   const uint32_t worker = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);

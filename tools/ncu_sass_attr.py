@@ -32,7 +32,8 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
-ai, si = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
+ai = hdr.index("Address")
+si = hdr.index("Instructions Executed" if "--inst" in sys.argv else "Warp Stall Sampling (All Samples)")
 samples = []
 for r in rows[2:]:
     if len(r) > si and r[ai].startswith("0x"):
