@@ -254,6 +254,8 @@ struct SnapStore {
   uint64_t cap = 0;
   char* img = nullptr;          // snapshot images (ImgHdr layout), rebuilt whenever the store changes
   uint64_t* img_off = nullptr;
+  uint64_t img_cap = 0;         // allocated bytes of img / entries of img_off (reused when large enough)
+  uint32_t img_off_cap = 0;
   void release() {
     cudaFree(nodes); cudaFree(pidx); cudaFree(off); cudaFree(n); cudaFree(nid);
     cudaFree(img); cudaFree(img_off);
@@ -284,6 +286,8 @@ struct mc_ctx {
   double* d_alphas = nullptr;  // small device buffer (64 entries)
   uint32_t* d_points = nullptr;  // live-pass snapshot points + first-eviction outputs
   uint32_t alpha_cap = 0;
+  char* img_scratch = nullptr;   // image_kernel workspace slices (zeroed once, reused: generation tags)
+  uint64_t img_scratch_bytes = 0;
 };
 
 namespace {
@@ -327,32 +331,61 @@ mc_status upload_stores(mc_ctx* c) {
 uint32_t default_workers(const mc_ctx* c) { return (uint32_t)(c->n_sm * c->blocks_per_sm * kWarpsPerCta); }
 
 // (Re)build the loadable images of variant v's snapshots (setup-time; allocates).
-mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st) {
+// host_n: the snapshot sizes when the caller knows them (else read back from the store).
+// Buffers are kept across calls and grown only when too small (no allocation on the
+// steady-state upload path).
+mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st, const uint32_t* host_n = nullptr) {
   SnapStore& s = c->snaps[v];
-  cudaFree(s.img);
-  cudaFree(s.img_off);
-  s.img = nullptr;
-  s.img_off = nullptr;
-  if (s.count == 0) return upload_stores(c);
+  if (s.count == 0) {
+    cudaFree(s.img);
+    cudaFree(s.img_off);
+    s.img = nullptr;
+    s.img_off = nullptr;
+    s.img_cap = 0;
+    s.img_off_cap = 0;
+    return upload_stores(c);
+  }
   std::vector<uint32_t> n(s.count);
-  CU(cudaMemcpyAsync(n.data(), s.n, sizeof(uint32_t) * s.count, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  if (host_n) {
+    std::copy(host_n, host_n + s.count, n.begin());
+  } else {
+    CU(cudaMemcpyAsync(n.data(), s.n, sizeof(uint32_t) * s.count, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
   std::vector<uint64_t> off(s.count + 1, 0);
   for (uint32_t k = 0; k < s.count; k++) {
     if (n[k] + 1 > c->ncap) return fail(MC_EOVERFLOW, "snapshot larger than max_nodes");
     off[k + 1] = off[k] + ((img_bytes(n[k]) + 255) & ~255ull);
   }
-  if (cudaMalloc(&s.img, off[s.count]) != cudaSuccess ||
-      cudaMalloc(&s.img_off, sizeof(uint64_t) * (s.count + 1)) != cudaSuccess)
-    return fail(MC_ENOMEM, "snapshot image allocation failed");
+  if (s.img_cap < off[s.count] || s.img_off_cap < s.count + 1) {
+    CU(cudaStreamSynchronize(st));  // the old images may still be read by queued work
+    cudaFree(s.img);
+    cudaFree(s.img_off);
+    s.img = nullptr;
+    s.img_off = nullptr;
+    s.img_cap = 0;
+    s.img_off_cap = 0;
+    if (cudaMalloc(&s.img, off[s.count]) != cudaSuccess ||
+        cudaMalloc(&s.img_off, sizeof(uint64_t) * (s.count + 1)) != cudaSuccess)
+      return fail(MC_ENOMEM, "snapshot image allocation failed");
+    s.img_cap = off[s.count];
+    s.img_off_cap = s.count + 1;
+  }
   CU(cudaMemcpyAsync(s.img_off, off.data(), sizeof(uint64_t) * (s.count + 1), cudaMemcpyHostToDevice, st));
   mc_status rc = upload_stores(c);
   if (rc != MC_OK) return rc;
   const uint32_t nb = std::min<uint32_t>(s.count, 4u * (uint32_t)c->n_sm);
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
-  char* scratch = nullptr;
-  if (cudaMalloc(&scratch, per * nb) != cudaSuccess) return fail(MC_ENOMEM, "image scratch allocation failed");
-  CU(cudaMemsetAsync(scratch, 0, per * nb, st));  // slices start zeroed (generation header)
+  if (c->img_scratch_bytes < per * nb) {
+    CU(cudaStreamSynchronize(st));
+    cudaFree(c->img_scratch);
+    c->img_scratch = nullptr;
+    c->img_scratch_bytes = 0;
+    if (cudaMalloc(&c->img_scratch, per * nb) != cudaSuccess) return fail(MC_ENOMEM, "image scratch allocation failed");
+    c->img_scratch_bytes = per * nb;
+    CU(cudaMemsetAsync(c->img_scratch, 0, per * nb, st));  // slices start zeroed (generation header)
+  }
+  char* scratch = c->img_scratch;
   KParams P;
   memset(&P, 0, sizeof(P));
   P.tok = c->tok;
@@ -370,8 +403,6 @@ mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st) {
   P.status = c->d_status;
   image_kernel<<<nb, 32, 0, st>>>(P, v, s.img, s.img_off);
   const cudaError_t e = cudaGetLastError();
-  cudaStreamSynchronize(st);
-  cudaFree(scratch);
   if (e != cudaSuccess) return fail(MC_ECUDA, std::string("image_kernel: ") + cudaGetErrorString(e));
   return MC_OK;
 }
@@ -465,6 +496,7 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
 void mc_destroy(mc_ctx* c) {
   if (!c) return;
   for (auto& s : c->snaps) s.release();
+  cudaFree(c->img_scratch);
   cudaFree(c->d_var);
   cudaFree(c->d_stores);
   cudaFree(c->d_segs);
@@ -561,7 +593,7 @@ mc_status mc_set_snapshots(mc_ctx* c, uint32_t variant, const mc_snap_node* h_no
   s.count = n_snap;
   mc_status rc = upload_stores(c);
   if (rc != MC_OK) return rc;
-  return build_images(c, variant, st);
+  return build_images(c, variant, st, cnt.data());
 }
 
 mc_status mc_workspace_size(const mc_ctx* c, uint32_t n_workers, uint32_t n_alpha, uint32_t n_chains,

@@ -690,17 +690,25 @@ __device__ void export_image(Chain& C, char* dst) {
   uint32_t* tpos = (uint32_t*)(dst + img_off_tpos(n));
   HEnt* tent = (HEnt*)(dst + img_off_tent(n));
   uint32_t w = 0;
-  for (uint32_t base = 0; base <= C.hmask; base += 32) {
-    const uint32_t j = base + lane;
-    const HEnt e = C.w.tab()[j];
-    const bool occ = hvalid(C, e.key);
-    const unsigned b = __ballot_sync(FULL, occ);
-    if (occ) {
-      const uint32_t k = w + __popc(b & ((1u << lane) - 1u));
-      tpos[k] = j;
-      tent[k] = e;
+  for (uint32_t base = 0; base <= C.hmask; base += 128) {  // 4 loads in flight per lane
+    HEnt e[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t j = base + 32 * q + lane;
+      if (j <= C.hmask) e[q] = C.w.tab()[j]; else e[q].key = 0;
     }
-    w += __popc(b);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t j = base + 32 * q + lane;
+      const bool occ = hvalid(C, e[q].key);
+      const unsigned b = __ballot_sync(FULL, occ);
+      if (occ) {
+        const uint32_t k = w + __popc(b & ((1u << lane) - 1u));
+        tpos[k] = j;
+        tent[k] = e[q];
+      }
+      w += __popc(b);
+    }
   }
   if (lane == 0) {
     ImgHdr h;

@@ -191,16 +191,28 @@ class Context:
         return t, d_r
 
     # ---- snapshots ----
-    def set_snapshots(self, variant: int, snapshots, stream=None):
-        """snapshots: list of (nodes structured array with SNAP_DTYPE fields, next_id)."""
+    @staticmethod
+    def pack_snapshots(snapshots):
+        """list of (nodes, next_id) -> (nodes SNAP_DTYPE[total], offsets u64[k+1], next_id u32[k])."""
         nodes = np.concatenate([np.asarray(s[0]).astype(SNAP_DTYPE) for s in snapshots]) \
             if snapshots else np.zeros(0, SNAP_DTYPE)
         nodes = np.ascontiguousarray(nodes, SNAP_DTYPE)
         off = np.zeros(len(snapshots) + 1, np.uint64)
         off[1:] = np.cumsum([len(s[0]) for s in snapshots])
         nid = np.asarray([s[1] for s in snapshots], np.uint32)
+        return nodes, off, nid
+
+    def set_snapshots(self, variant: int, snapshots, stream=None):
+        """snapshots: list of (nodes structured array with SNAP_DTYPE fields, next_id)."""
+        self.set_snapshots_packed(variant, *self.pack_snapshots(snapshots), stream=stream)
+
+    def set_snapshots_packed(self, variant: int, nodes, off, nid, stream=None):
+        """Packed host arrays (see pack_snapshots; nodes may live in pinned memory)."""
+        assert nodes.dtype == SNAP_DTYPE and nodes.flags.c_contiguous
+        off = np.ascontiguousarray(off, np.uint64)
+        nid = np.ascontiguousarray(nid, np.uint32)
         check(lib().mc_set_snapshots(self.h, variant, _np_ptr(nodes), _np_ptr(off), _np_ptr(nid),
-                                     len(snapshots), _stream_ptr(stream)))
+                                     len(nid), _stream_ptr(stream)))
 
     def snapshot_count(self, variant: int) -> int:
         n = C.c_uint32()
