@@ -73,9 +73,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const DevVariant V = P.var[v];
     const mc_segment seg = P.segs[s];
     Chain C;
-    chain_init(C, P, worker, V, P.alphas[a], smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes, P.smem_nodes);
-    // the policy is a compile-time constant in each instantiation
-    if (kPolicy == 0) { C.block = 0; C.mthr = 2; } else { C.mthr = 1; C.alpha = 0.0; }
+    // the warp's shared memory: dense slots [0, S - 8), then the chain constants (64 B)
+    char* sw = smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes;
+    chain_init(C, P, worker, V, P.alphas[a], sw, P.smem_nodes - 8,
+               reinterpret_cast<ChainConst*>(sw + 8ull * (P.smem_nodes - 8)));
+    // the policy is a compile-time constant in each instantiation (vLLM+ chains have
+    // block > 0, so chain_init already set their α to 0)
+    if (kPolicy == 0) { C.block = 0; C.mthr = 2; } else { C.mthr = 1; }
 #ifdef MC_LOAD_TIMER
     const long long _l0 = clock64();
 #endif
@@ -141,7 +145,8 @@ __global__ void __launch_bounds__(32) image_kernel(KParams P, uint32_t v, char* 
   const DevSnapStore& st = P.snap[v];
   for (uint32_t k = w; k < st.count; k += P.n_workers) {
     Chain C;
-    chain_init(C, P, w, P.var[v], 0.0, nullptr, 0);
+    __shared__ ChainConst kc;
+    chain_init(C, P, w, P.var[v], 0.0, nullptr, 0, &kc);
     load_snapshot(C, P, &st, k);
     export_image(C, img + img_off[k]);
   }
@@ -153,7 +158,8 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   const uint32_t v = blockIdx.x;
   if (v >= P.n_var) return;
   Chain C;
-  chain_init(C, P, v, P.var[v], 0.0, smem, P.smem_nodes);
+  chain_init(C, P, v, P.var[v], 0.0, smem, P.smem_nodes - 8,
+             reinterpret_cast<ChainConst*>(smem + 8ull * (P.smem_nodes - 8)));
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
@@ -822,6 +828,7 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   uint32_t S = A->smem_nodes ? A->smem_nodes : c->smem_nodes;
   S = std::min<uint32_t>(S, c->ncap) & ~31u;
   if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
+  if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (8 slots hold the chain constants)");
   P.smem_nodes = S;
   // one launch per policy group, back to back on `st` (they share the worker slices);
   // each launch has its own queue word

@@ -79,6 +79,15 @@ struct DevVariant {
   uint32_t cap_nodes, chunk;  // chunk = 0: exact checkpoints; else chunk-aligned prefill checkpoints
   uint32_t block, pad;        // block > 0: the vLLM+ baseline with token blocks of `block` (NEXT-2)
 };
+// Per-chain read-only constants, kept in the warp's shared memory (64 B) so that the
+// replay loop does not hold them in registers (the kernel runs at the 128-register cap).
+struct ChainConst {
+  DevModel m;
+  uint64_t capb;
+  uint32_t capn, chunk;
+  double alpha;
+};
+static_assert(sizeof(ChainConst) == 64, "ChainConst is carved from 8 dense slots");
 struct DevSnapStore {
   const mc_snap_node* nodes;
   const uint32_t* pidx;  // parent position within the same snapshot, NIL = root
@@ -285,12 +294,9 @@ struct Chain {
   uint32_t count;     // live non-root nodes (the dense list spans slots [0, hwm), holes included)
   uint64_t total;     // bytes of all live nodes
   uint32_t next_id, hwm, nfree;
-  DevModel m;
-  uint64_t capb;
-  uint32_t capn, chunk;
+  const ChainConst* K;  // the chain's read-only constants, in shared memory (not registers)
   uint32_t block;  // > 0: vLLM+ baseline (token blocks of `block`), else Marconi
   uint32_t mthr;   // D_MULTI threshold: children that make a node a non-candidate (2 Marconi, 1 vLLM+)
-  double alpha;
   uint64_t c_cmp, c_vis, c_scan, c_wr;
   uint32_t n_evict;   // evictions so far (uniform)
   // cached normalisation bounds (bc_valid bit 0: t and fp32 eff bounds exact; bits 1 / 2:
@@ -483,7 +489,7 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   const uint32_t i = s;
   C.count++;
   const NodeRec& R = C.w.rec()[s];
-  const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
+  const double v = node_eff(C.K->m, R.ds, R.de, (R.nf >> 24) & F_SSM);
   C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
   d->e32 = __double2float_rn(v);
@@ -588,7 +594,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     R.pad = 0;
     C.w.rec()[s] = R;
     C.w.ids()[s] = r.id;
-    bytes += node_bytes(C.m, r.d_start, r.d_end, r.has_ssm);
+    bytes += node_bytes(C.K->m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
   for (uint32_t i = lane; i < n; i += 32) {
@@ -617,7 +623,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   for (uint32_t i = lane; i < n; i += 32) {
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
-    const double v = node_eff(C.m, R.ds, R.de, (R.nf >> 24) & F_SSM);
+    const double v = node_eff(C.K->m, R.ds, R.de, (R.nf >> 24) & F_SSM);
     C.w.eff64()[s] = v;
     DenseRec* d = d_ptr(C, s);
     d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
@@ -1003,7 +1009,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   Best best;
   best_init(best);
   bounds_init(b);
-  if (C.alpha == 0.0) {
+  if (C.K->alpha == 0.0) {
     scan_dense(C, cnt, [&](int, uint32_t i, uint32_t tc, float) {
       const uint32_t t = tc & T_MASK;
       b.tmin = min(b.tmin, t);
@@ -1104,7 +1110,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   const bool dt0 = tmax == tmin;
   const double de32 = (double)hi32 - (double)lo32;  // exact in fp64
   const float idt = dt0 ? 0.0f : __frcp_rn((float)(tmax - tmin));
-  const float aide = (de32 == 0.0) ? 0.0f : __double2float_rn(__ddiv_rn(C.alpha, de32));
+  const float aide = (de32 == 0.0) ? 0.0f : __double2float_rn(__ddiv_rn(C.K->alpha, de32));
   const float INF = __int_as_float(0x7F800000);
   const double* __restrict__ e64 = C.w.eff64();
   float a1[kUnroll], a2[kUnroll];
@@ -1144,7 +1150,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   if (de32 == 0.0) ENSURE_EXTREMES();
   const bool exact_only = (de32 == 0.0) && (b.emax != b.emin);
   const double ratio = (de32 == 0.0) ? 0.0 : __ddiv_rn((double)hi32, de32);
-  const double delta = 1.9073486328125e-06 * (1.0 + C.alpha * (1.0 + 4.0 * ratio));
+  const double delta = 1.9073486328125e-06 * (1.0 + C.K->alpha * (1.0 + 4.0 * ratio));
   const double lim = (double)kmin + delta;
   if (!exact_only && !__any_sync(FULL, (double)k2 <= lim)) {
     const bool mine = (double)k1 <= lim;
@@ -1156,7 +1162,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.id = NIL;
       if (need_u) {  // the exact utility is only logged (no global read otherwise)
         ENSURE_EXTREMES();
-        if (mine) best.u = utility(b, d_tc(C, i1), e64[i1], C.alpha);
+        if (mine) best.u = utility(b, d_tc(C, i1), e64[i1], C.K->alpha);
         best.u = __shfl_sync(FULL, best.u, src);
       }
       return best;
@@ -1164,7 +1170,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     ENSURE_EXTREMES();
     if (mine) {  // near-ties: exact utilities, ids for exact ties
       best.t = d_tc(C, i1);
-      best.u = utility(b, best.t, e64[i1], C.alpha);
+      best.u = utility(b, best.t, e64[i1], C.K->alpha);
       best.i = i1;
       best.slot = i1;
       best.id = d_id(C, i1);
@@ -1178,7 +1184,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   // near-ties / unresolvable fp32 range: exact full pass (cold path)
   ENSURE_EXTREMES();
 #undef ENSURE_EXTREMES
-  return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.alpha);
+  return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.K->alpha);
 }
 
 __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
@@ -1212,7 +1218,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     uint32_t kind;
     if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
       kind = 0;
-      C.total -= node_bytes(C.m, X.ds, X.de, xf & F_SSM);
+      C.total -= node_bytes(C.K->m, X.ds, X.de, xf & F_SSM);
       hash_erase_at_1(C, X.hidx);
       NodeRec& Wp = C.w.rec()[p];
       Wp.nf = Rp.nf - 1;
@@ -1226,7 +1232,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       const uint32_t hc = Rc.hidx;   // entry of c under x (erased)
       const uint32_t hx = X.hidx;    // entry of x under p (becomes c's: same key)
       const uint32_t xtok = C.w.tab()[hx].tok;
-      if (xf & F_SSM) C.total -= C.m.ssmb;
+      if (xf & F_SSM) C.total -= C.K->m.ssmb;
       NodeRec& Wc = C.w.rec()[c];
       Wc.ds = X.ds;
       Wc.parent = p;
@@ -1234,7 +1240,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       C.w.tab()[hx] = hmake(C, p, xtok, c, Rc.de, (Rc.nf >> 24) & F_SSM, Rc.roff);
       hash_erase_at_1(C, hc);
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
-      const double ec = node_eff(C.m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
+      const double ec = node_eff(C.K->m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
       d_set_eff(C, c, ec);
       C.c_wr += 2;
     }
@@ -1283,7 +1289,7 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   Ry.hidx = hash_insert_1(C, hmake(C, u, ft, y, Y.de, (Y.nf >> 24) & F_SSM, Y.roff), u);
   C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
-  d_set_eff(C, y, node_eff(C.m, x, Y.de, (Y.nf >> 24) & F_SSM));
+  d_set_eff(C, y, node_eff(C.K->m, x, Y.de, (Y.nf >> 24) & F_SSM));
   C.c_wr += 2;
   return u;
 }
@@ -1293,7 +1299,7 @@ __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   const uint32_t nf = R.nf, dp = x, ds = R.ds, de = R.de, hi = R.hidx;
   R.nf = nf | (F_SSM << 24);
   C.w.tab()[hi].de = de | 0x80000000u;  // the child index carries the state flag for the walk
-  d_set_eff(C, dp, node_eff(C.m, ds, de, true));
+  d_set_eff(C, dp, node_eff(C.K->m, ds, de, true));
   d_stamp(C, dp, r);
   C.c_wr += 1;
 }
@@ -1364,7 +1370,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
       my_dp = c;  // dense position = slot
     }
     npath++;
-    pinned_bytes += node_bytes(C.m, pos, de, fl & F_SSM);
+    pinned_bytes += node_bytes(C.K->m, pos, de, fl & F_SSM);
     if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
     if (k == len) {
       v = c;
@@ -1391,7 +1397,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   }
 
   // Step 2: pure Transformer (n_ssm = 0): KVs can be sliced mid-edge.
-  if (C.m.n_ssm == 0) {
+  if (C.K->m.n_ssm == 0) {
     reuse = min(m, L_in);
     hit = NIL;
     hit_idx = NIL;
@@ -1444,8 +1450,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   }
   // Chunked state passing (NEXT-3): the prefill checkpoint moves down to the
   // chunk boundary at or below the branch point; skipped if that is 0 or not beyond the hit.
-  if (C.chunk && p) {
-    uint32_t pa = (p / C.chunk) * C.chunk;
+  if (C.K->chunk && p) {
+    uint32_t pa = (p / C.K->chunk) * C.K->chunk;
     if (pa == 0 || pa <= reuse) pa = 0;
     p_split = NIL;
     p_gain = NIL;
@@ -1485,16 +1491,16 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   if (partial == NIL && m == n && n != p && !(v_flags & F_SSM)) n_gain = v;
   uint32_t n_ck = p ? 1u : 0u;
   if (n != p && (leaf || split_n || n_gain != NIL)) n_ck++;
-  const uint64_t d_bytes = C.m.kvt * (uint64_t)(n - m) + C.m.ssmb * n_ck;
+  const uint64_t d_bytes = C.K->m.kvt * (uint64_t)(n - m) + C.K->m.ssmb * n_ck;
   const uint32_t d_nodes = (p_split != NIL ? 1u : 0u) + (split_m ? 1u : 0u) + (split_n ? 1u : 0u) + (leaf ? 1u : 0u);
 
   PHASE_MARK(C.t_walk);
 
   // Step 6: admission precheck (R12).
-  const bool bypass = (pinned_bytes + d_bytes > C.capb) || (C.capn && npath + d_nodes > C.capn);
+  const bool bypass = (pinned_bytes + d_bytes > C.K->capb) || (C.K->capn && npath + d_nodes > C.K->capn);
   if (!bypass) {
     // Step 7: evict the argmin utility until the request fits.
-    while (!C.failed && (C.total + d_bytes > C.capb || (C.capn && C.count + d_nodes > C.capn))) {
+    while (!C.failed && (C.total + d_bytes > C.K->capb || (C.K->capn && C.count + d_nodes > C.K->capn))) {
       evict_one(C, P, r, log, log_n);
     }
     PHASE_MARK(C.t_evict);
@@ -1542,7 +1548,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
         if (n_gain == NIL && p_gain != v) C.c_wr += 1;
       }
       C.total += d_bytes;
-      if (C.total > C.capb || (C.capn && C.count > C.capn)) {
+      if (C.total > C.K->capb || (C.K->capn && C.count > C.K->capn)) {
         atomicOr(P.status, ST_INVARIANT);
         C.failed = true;
       }
@@ -1569,7 +1575,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   PHASE_MARK(C.t_unpin);
   ReqOut o;
   o.reuse = reuse;
-  o.flops = prefill_F(C.m, reuse);
+  o.flops = prefill_F(C.K->m, reuse);
   o.bypass = bypass;
   return o;
 }
@@ -1683,7 +1689,7 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
         const NodeRec X = C.w.rec()[x];
         const uint32_t p = X.parent;
         const NodeRec Rp = C.w.rec()[p];
-        C.total -= node_bytes(C.m, X.ds, X.de, (X.nf >> 24) & F_SSM);
+        C.total -= node_bytes(C.K->m, X.ds, X.de, (X.nf >> 24) & F_SSM);
         hash_erase_at_1(C, X.hidx);
         NodeRec& Wp = C.w.rec()[p];
         Wp.nf = Rp.nf - 1;
@@ -1804,16 +1810,16 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   __syncwarp();
 
   // Step 4: admission (V7): bypass when the matched path plus the new blocks exceed the capacity.
-  const uint64_t bb = node_bytes(C.m, 0, x, true);
+  const uint64_t bb = node_bytes(C.K->m, 0, x, true);
   const uint32_t n_new = nb - mb;
   const uint64_t d_bytes = bb * n_new;
-  const bool bypass = (bb * mb + d_bytes > C.capb) || (C.capn && nb > C.capn);
+  const bool bypass = (bb * mb + d_bytes > C.K->capb) || (C.K->capn && nb > C.K->capn);
   if (!bypass) {
     // Step 5: LRU leaf eviction (V6) until the new blocks fit; every block has the same
     // size, so the number of victims is known up front.
     uint64_t need = 0;
-    if (C.total + d_bytes > C.capb) need = (C.total + d_bytes - C.capb + bb - 1) / bb;
-    if (C.capn && C.count + n_new > C.capn) need = max(need, (uint64_t)(C.count + n_new - C.capn));
+    if (C.total + d_bytes > C.K->capb) need = (C.total + d_bytes - C.K->capb + bb - 1) / bb;
+    if (C.K->capn && C.count + n_new > C.K->capn) need = max(need, (uint64_t)(C.count + n_new - C.K->capn));
     if (need) evict_lru_blocks(C, P, r, (uint32_t)need, log, log_n);
     // Step 6: insert blocks mb .. nb-1 under v, in parallel (one block per lane).
     if (n_new && !C.failed) {
@@ -1873,7 +1879,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           C.next_id = id0 + n_new;
           C.total += d_bytes;
           C.c_wr += n_new;
-          if (C.total > C.capb || (C.capn && C.count > C.capn)) {
+          if (C.total > C.K->capb || (C.K->capn && C.count > C.K->capn)) {
             atomicOr(P.status, ST_INVARIANT);
             C.failed = true;
           }
@@ -1890,13 +1896,14 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   __syncwarp();
   ReqOut o;
   o.reuse = reuse;
-  o.flops = prefill_F(C.m, reuse);
+  o.flops = prefill_F(C.K->m, reuse);
   o.bypass = bypass;
   return o;
 }
 
+// kc: 64 B of shared memory for the chain's constants (written by lane 0 here).
 __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t worker, const DevVariant& V,
-                                           double alpha, char* smem_warp, uint32_t S) {
+                                           double alpha, char* smem_warp, uint32_t S, ChainConst* kc) {
   C.w.b = P.ws + (uint64_t)worker * P.ws_stride;
   C.w.n = P.ncap;
   C.w.h = P.hcap;
@@ -1905,13 +1912,17 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
   C.ncap = P.ncap;
   C.hmask = P.hcap - 1;
   C.gen = 0;
-  C.m = V.m;
-  C.capb = V.cap_bytes;
-  C.capn = V.cap_nodes;
-  C.chunk = V.chunk;
+  if (lane_id() == 0) {
+    kc->m = V.m;
+    kc->capb = V.cap_bytes;
+    kc->capn = V.cap_nodes;
+    kc->chunk = V.chunk;
+    kc->alpha = V.block ? 0.0 : alpha;  // vLLM+ is LRU: α does not apply
+  }
+  __syncwarp();
+  C.K = kc;
   C.block = V.block;
   C.mthr = V.block ? 1u : 2u;  // vLLM+ evicts leaf blocks only (V6)
-  C.alpha = V.block ? 0.0 : alpha;  // vLLM+ is LRU: α does not apply
   C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;
   C.bc_valid = 0;
