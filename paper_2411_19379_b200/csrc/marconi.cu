@@ -73,10 +73,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const DevVariant V = P.var[v];
     const mc_segment seg = P.segs[s];
     Chain C;
-    // the warp's shared memory: dense slots [0, S - 8), then the chain constants (64 B)
+    // the warp's shared memory: dense slots [0, S - 12), the counters (32 B), the chain
+    // constants (64 B)
     char* sw = smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes;
-    chain_init(C, P, worker, V, P.alphas[a], sw, P.smem_nodes - 8,
-               reinterpret_cast<ChainConst*>(sw + 8ull * (P.smem_nodes - 8)));
+    const uint32_t S = P.smem_nodes - kSmemReserved;
+    chain_init(C, P, worker, V, P.alphas[a], sw, S, reinterpret_cast<ChainConst*>(sw + 8ull * (S + 4)),
+               reinterpret_cast<ChainCtr*>(sw + 8ull * S));
     // the policy is a compile-time constant in each instantiation (vLLM+ chains have
     // block > 0, so chain_init already set their α to 0)
     if (kPolicy == 0) { C.block = 0; C.mthr = 2; } else { C.mthr = 1; }
@@ -114,10 +116,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
         P.counters[4ull * c + 2] = C.t_insert;
         P.counters[4ull * c + 3] = C.t_unpin;
 #else
-        P.counters[4ull * c + 0] = C.c_cmp;
-        P.counters[4ull * c + 1] = C.c_vis;
-        P.counters[4ull * c + 2] = C.c_scan;
-        P.counters[4ull * c + 3] = C.c_wr;
+        P.counters[4ull * c + 0] = C.X->cmp;
+        P.counters[4ull * c + 1] = C.X->vis;
+        P.counters[4ull * c + 2] = C.X->scan;
+        P.counters[4ull * c + 3] = C.X->wr;
 #ifdef MC_LOAD_TIMER
         P.counters[4ull * c + 0] = (unsigned long long)(_l1 - _l0);
 #endif
@@ -146,7 +148,8 @@ __global__ void __launch_bounds__(32) image_kernel(KParams P, uint32_t v, char* 
   for (uint32_t k = w; k < st.count; k += P.n_workers) {
     Chain C;
     __shared__ ChainConst kc;
-    chain_init(C, P, w, P.var[v], 0.0, nullptr, 0, &kc);
+    __shared__ ChainCtr kx;
+    chain_init(C, P, w, P.var[v], 0.0, nullptr, 0, &kc, &kx);
     load_snapshot(C, P, &st, k);
     export_image(C, img + img_off[k]);
   }
@@ -158,8 +161,9 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   const uint32_t v = blockIdx.x;
   if (v >= P.n_var) return;
   Chain C;
-  chain_init(C, P, v, P.var[v], 0.0, smem, P.smem_nodes - 8,
-             reinterpret_cast<ChainConst*>(smem + 8ull * (P.smem_nodes - 8)));
+  const uint32_t S = P.smem_nodes - kSmemReserved;
+  chain_init(C, P, v, P.var[v], 0.0, smem, S, reinterpret_cast<ChainConst*>(smem + 8ull * (S + 4)),
+             reinterpret_cast<ChainCtr*>(smem + 8ull * S));
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
@@ -828,7 +832,7 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   uint32_t S = A->smem_nodes ? A->smem_nodes : c->smem_nodes;
   S = std::min<uint32_t>(S, c->ncap) & ~31u;
   if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
-  if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (8 slots hold the chain constants)");
+  if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (12 slots hold the chain counters and constants)");
   P.smem_nodes = S;
   // one launch per policy group, back to back on `st` (they share the worker slices);
   // each launch has its own queue word

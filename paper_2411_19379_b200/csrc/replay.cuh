@@ -88,6 +88,13 @@ struct ChainConst {
   double alpha;
 };
 static_assert(sizeof(ChainConst) == 64, "ChainConst is carved from 8 dense slots");
+// Per-chain algorithmic counters, lane 0 accumulates them in shared
+// memory (read once, at the end of the chain).
+struct ChainCtr {
+  uint64_t cmp, vis, scan, wr;
+};
+static_assert(sizeof(ChainCtr) == 32, "ChainCtr is carved from 4 dense slots");
+constexpr uint32_t kSmemReserved = 12;  // dense slots per warp holding ChainCtr + ChainConst
 struct DevSnapStore {
   const mc_snap_node* nodes;
   const uint32_t* pidx;  // parent position within the same snapshot, NIL = root
@@ -204,6 +211,10 @@ struct WS {
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+#define CTR_ADD(C, f, v)                      \
+  do {                                        \
+    if (lane_id() == 0) (C).X->f += (v);      \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // K1: cost model (Eq. 1 with Appendix A), bit-exact with the host definition.
@@ -297,7 +308,7 @@ struct Chain {
   const ChainConst* K;  // the chain's read-only constants, in shared memory (not registers)
   uint32_t block;  // > 0: vLLM+ baseline (token blocks of `block`), else Marconi
   uint32_t mthr;   // D_MULTI threshold: children that make a node a non-candidate (2 Marconi, 1 vLLM+)
-  uint64_t c_cmp, c_vis, c_scan, c_wr;
+  ChainCtr* X;  // counters (shared memory, lane 0 writes)
   uint32_t n_evict;   // evictions so far (uniform)
   // cached normalisation bounds (bc_valid bit 0: t and fp32 eff bounds exact; bits 1 / 2:
   // bc_elo / bc_ehi also exact -- recovered lazily, only a logged or near-tied victim
@@ -321,7 +332,6 @@ __device__ __forceinline__ void sync_state(Chain& C) {
   C.next_id = __shfl_sync(FULL, C.next_id, 0);
   C.hwm = __shfl_sync(FULL, C.hwm, 0);
   C.nfree = __shfl_sync(FULL, C.nfree, 0);
-  C.c_wr = __shfl_sync(FULL, (unsigned long long)C.c_wr, 0);
   C.failed = __shfl_sync(FULL, (int)C.failed, 0);
   C.bc_valid = __shfl_sync(FULL, C.bc_valid, 0);
   C.bc_tmin = __shfl_sync(FULL, C.bc_tmin, 0);
@@ -1198,7 +1208,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
 #ifdef MC_PHASE_TIMERS3
   { long long _n = clock64(); C.t_walk += (unsigned long long)(_n - _e3); _e3 = _n; }
 #endif
-  C.c_scan += cnt;
+  CTR_ADD(C, scan, cnt);
   C.n_evict++;
   if (best.i == NIL) {
     if (lane == 0) atomicOr(P.status, ST_NOCAND);
@@ -1224,7 +1234,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       Wp.nf = Rp.nf - 1;
       Wp.cxor = Rp.cxor ^ x;
       if (p != 0) d_multi(C, p, (Rp.nf & NCH_MASK) - 1);
-      C.c_wr += 1;
+      CTR_ADD(C, wr, 1);
     } else {  // one child: release the state, the child absorbs the KVs
       kind = 1;
       const uint32_t c = X.cxor;
@@ -1242,7 +1252,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
       C.w.rec()[p].cxor = Rp.cxor ^ x ^ c;
       const double ec = node_eff(C.K->m, X.ds, Rc.de, (Rc.nf >> 24) & F_SSM);
       d_set_eff(C, c, ec);
-      C.c_wr += 2;
+      CTR_ADD(C, wr, 2);
     }
     if (log) {
       const uint32_t li = *log_n;
@@ -1290,7 +1300,7 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   C.w.rec()[Y.parent].cxor = cx ^ y ^ u;
   dense_add_1(C, u, r);
   d_set_eff(C, y, node_eff(C.K->m, x, Y.de, (Y.nf >> 24) & F_SSM));
-  C.c_wr += 2;
+  CTR_ADD(C, wr, 2);
   return u;
 }
 
@@ -1301,7 +1311,7 @@ __device__ __forceinline__ void gain_1(Chain& C, uint32_t x, uint32_t r) {
   C.w.tab()[hi].de = de | 0x80000000u;  // the child index carries the state flag for the walk
   d_set_eff(C, dp, node_eff(C.K->m, ds, de, true));
   d_stamp(C, dp, r);
-  C.c_wr += 1;
+  CTR_ADD(C, wr, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1386,8 +1396,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     }
   }
   __syncwarp();
-  C.c_cmp += min(m + 1, n);
-  C.c_vis += npath + 1;
+  CTR_ADD(C, cmp, min(m + 1, n));
+  CTR_ADD(C, vis, npath + 1);
   if (has_next) {
     nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
     if (lane == 0) {
@@ -1423,7 +1433,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
       d->tc = (i == hit_idx ? (r | (d->tc & D_MULTI)) : d->tc) | D_PIN;
     }
   if (hit != NIL) {
-    C.c_wr += 1;
+    CTR_ADD(C, wr, 1);
     old_t = __shfl_sync(FULL, old_t, hit_idx < 32 ? hit_idx : 0);
     bc_change_t(C, old_t, r);  // uniform: every lane updates its copy of the bound cache
   }
@@ -1540,12 +1550,12 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
           Wa.cxor = Ra.cxor ^ w;
           if (attach != 0) d_multi(C, attach, (Ra.nf & NCH_MASK) + 1);
           dense_add_1(C, w, r);
-          C.c_wr += 1;
+          CTR_ADD(C, wr, 1);
         }
       } else if (partial == NIL) {
         // final node at n already exists: timestamp it (R5)
         d_stamp(C, v, r);
-        if (n_gain == NIL && p_gain != v) C.c_wr += 1;
+        if (n_gain == NIL && p_gain != v) CTR_ADD(C, wr, 1);
       }
       C.total += d_bytes;
       if (C.total > C.K->capb || (C.K->capn && C.count > C.K->capn)) {
@@ -1709,7 +1719,7 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
         C.count = last;
         C.w.rec()[x].nf = 0;
         C.w.freel()[C.nfree++] = x;
-        C.c_wr += 1;
+        CTR_ADD(C, wr, 1);
         if (p != 0 && (Rp.nf & NCH_MASK) == 1) {  // the parent lost its last child
           const uint32_t pp = p;
           const DenseRec dp = *d_ptr(C, pp);
@@ -1720,7 +1730,7 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
         }
       }
       sync_state(C);
-      C.c_scan += cnt;
+      CTR_ADD(C, scan, cnt);
       C.n_evict++;
       need--;
       progressed = true;
@@ -1787,8 +1797,8 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
     }
   }
   __syncwarp();
-  C.c_cmp += (uint64_t)mb * x;
-  C.c_vis += mb + 1;
+  CTR_ADD(C, cmp, (uint64_t)mb * x);
+  CTR_ADD(C, vis, mb + 1);
   if (has_next) nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
 
   // Step 2: hit = the deepest matched block end <= L_in (V4).
@@ -1806,7 +1816,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
     DenseRec* d = d_ptr(C, path[i]);
     d->tc = r | (d->tc & D_MULTI) | D_PIN;
   }
-  C.c_wr += mb;
+  CTR_ADD(C, wr, mb);
   __syncwarp();
 
   // Step 4: admission (V7): bypass when the matched path plus the new blocks exceed the capacity.
@@ -1878,7 +1888,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           C.count = cnt0 + n_new;
           C.next_id = id0 + n_new;
           C.total += d_bytes;
-          C.c_wr += n_new;
+          CTR_ADD(C, wr, n_new);
           if (C.total > C.K->capb || (C.K->capn && C.count > C.K->capn)) {
             atomicOr(P.status, ST_INVARIANT);
             C.failed = true;
@@ -1901,9 +1911,9 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   return o;
 }
 
-// kc: 64 B of shared memory for the chain's constants (written by lane 0 here).
+// kc / kx: shared memory for the chain's constants and counters (written by lane 0 here).
 __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t worker, const DevVariant& V,
-                                           double alpha, char* smem_warp, uint32_t S, ChainConst* kc) {
+                                           double alpha, char* smem_warp, uint32_t S, ChainConst* kc, ChainCtr* kx) {
   C.w.b = P.ws + (uint64_t)worker * P.ws_stride;
   C.w.n = P.ncap;
   C.w.h = P.hcap;
@@ -1918,12 +1928,13 @@ __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t 
     kc->capn = V.cap_nodes;
     kc->chunk = V.chunk;
     kc->alpha = V.block ? 0.0 : alpha;  // vLLM+ is LRU: α does not apply
+    kx->cmp = kx->vis = kx->scan = kx->wr = 0;
   }
   __syncwarp();
   C.K = kc;
+  C.X = kx;
   C.block = V.block;
   C.mthr = V.block ? 1u : 2u;  // vLLM+ evicts leaf blocks only (V6)
-  C.c_cmp = C.c_vis = C.c_scan = C.c_wr = 0;
   C.n_evict = 0;
   C.bc_valid = 0;
   C.bc_tmin = 0; C.bc_tmax = 0; C.bc_lo = 0.0f; C.bc_hi = 0.0f; C.bc_elo = 0.0; C.bc_ehi = 0.0;
