@@ -1006,6 +1006,25 @@ __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* ta
   return best;
 }
 
+// α = 0 with the oldest t shared by several candidates: the one with the smallest id.
+__device__ __noinline__ uint32_t lru_tiebreak(const DenseRec* sd, const DenseRec* tail, const uint32_t* ids,
+                                              uint32_t cnt, uint32_t S, uint32_t t) {
+  const uint32_t lane = lane_id();
+  uint32_t bid = 0xFFFFFFFFu, bi = NIL;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint32_t tc = (i < S ? sd[i] : tail[i]).tc;
+    if (!(tc & D_FLAGS) && tc == t) {
+      const uint32_t id = ids[i];
+      if (id < bid) { bid = id; bi = i; }
+    }
+  }
+  uint32_t m = bid;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+  const unsigned w = __ballot_sync(FULL, bid == m && bi != NIL);
+  return __shfl_sync(FULL, bi, __ffs(w) - 1);
+}
+
 // Exact victim selection over the dense live list (Eq. 2).
 //   α = 0: u = rec exactly and rec is strictly monotone in t, so the victim is the
 //          candidate with the smallest (t_last, id) -- one integer pass (LRU).
@@ -1020,46 +1039,52 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   best_init(best);
   bounds_init(b);
   if (C.K->alpha == 0.0) {
-    scan_dense(C, cnt, [&](int, uint32_t i, uint32_t tc, float) {
+    // One branch-free pass: per unroll slot the smallest candidate t, its slot and whether
+    // another candidate shares that t; ids are read only when the minimum t is tied.
+    uint32_t bt[kUnroll], bi[kUnroll], tmn[kUnroll], tmx[kUnroll];
+    bool tie[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; q++) {
+      bt[q] = 0xFFFFFFFFu; bi[q] = NIL; tmn[q] = 0xFFFFFFFFu; tmx[q] = 0; tie[q] = false;
+    }
+    scan_dense(C, cnt, [&](int q, uint32_t i, uint32_t tc, float) {
       const uint32_t t = tc & T_MASK;
-      b.tmin = min(b.tmin, t);
-      b.tmax = max(b.tmax, tc == HOLE_TC ? 0u : t);
-      if (!(tc & D_FLAGS) && t <= best.t) {
-        if (t < best.t) {
-          best.t = t; best.i = i; best.id = NIL;  // id fetched lazily on a t tie
-        } else {
-          if (best.id == NIL) best.id = d_id(C, best.i);
-          const uint32_t id = d_id(C, i);
-          if (id < best.id) { best.i = i; best.id = id; }
-        }
-      }
+      tmn[q] = min(tmn[q], t);
+      tmx[q] = max(tmx[q], tc == HOLE_TC ? 0u : t);
+      const uint32_t k = (tc & D_FLAGS) ? 0xFFFFFFFFu : t;  // non-candidates never win
+      const bool lt = k < bt[q];
+      tie[q] = lt ? false : (tie[q] | (k == bt[q]));
+      bi[q] = lt ? i : bi[q];
+      bt[q] = lt ? k : bt[q];
     });
-    best.slot = best.i;  // for the removal
-    // resolve ids only when lanes tie on the minimum t
+    uint32_t t1 = bt[0], i1 = bi[0];
+    bool tied1 = tie[0];
+    b.tmin = tmn[0];
+    b.tmax = tmx[0];
+#pragma unroll
+    for (int q = 1; q < kUnroll; q++) {
+      b.tmin = min(b.tmin, tmn[q]);
+      b.tmax = max(b.tmax, tmx[q]);
+      if (bt[q] < t1) { t1 = bt[q]; i1 = bi[q]; tied1 = tie[q]; }
+      else if (bt[q] == t1) tied1 = true;
+    }
+    uint32_t tbest = t1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       b.tmin = min(b.tmin, __shfl_xor_sync(FULL, b.tmin, o));
       b.tmax = max(b.tmax, __shfl_xor_sync(FULL, b.tmax, o));
+      tbest = min(tbest, __shfl_xor_sync(FULL, tbest, o));
     }
-    uint32_t tbest = best.t;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tbest = min(tbest, __shfl_xor_sync(FULL, tbest, o));
-    const unsigned tied = __ballot_sync(FULL, best.i != NIL && best.t == tbest);
-    if (tied == 0) return best;
-    if (__popc(tied) > 1) {
-      if (best.i != NIL && best.t == tbest && best.id == NIL) best.id = d_id(C, best.i);
+    if (tbest == 0xFFFFFFFFu) return best;  // no candidate
+    const unsigned at = __ballot_sync(FULL, t1 == tbest);
+    const bool unique = __popc(at) == 1 && !__shfl_sync(FULL, (int)tied1, __ffs(at) - 1);
+    best.t = tbest;
+    if (unique) {
+      best.i = __shfl_sync(FULL, i1, __ffs(at) - 1);
+    } else {  // several candidates share the oldest t: smallest id (R4), cold path
+      best.i = lru_tiebreak(C.sd, C.w.tail(), C.w.ids(), cnt, C.S, tbest);
     }
-    if (best.t != tbest) { best.i = NIL; best.id = NIL; best.t = 0xFFFFFFFFu; best.slot = NIL; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const uint32_t t = __shfl_xor_sync(FULL, best.t, o);
-      const uint32_t id = __shfl_xor_sync(FULL, best.id, o);
-      const uint32_t i = __shfl_xor_sync(FULL, best.i, o);
-      const uint32_t sl = __shfl_xor_sync(FULL, best.slot, o);
-      if (i != NIL && (best.i == NIL || t < best.t || (t == best.t && id < best.id))) {
-        best.t = t; best.id = id; best.i = i; best.slot = sl;
-      }
-    }
+    best.slot = best.i;
     const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
     best.u = __dadd_rn(rec, __dmul_rn(0.0, 0.5));  // = rec (α·effn = +0)
     return best;
