@@ -71,8 +71,10 @@ if os.environ.get("PHASES3A"):
         nreq = ns * w.window
         sel, p2, rem = (sub[:, k].astype(np.float64).sum() / nreq / 1e3 for k in range(3))
         p1 = float((sub[:, 3] >> np.uint64(32)).sum()) / nreq
-        fb = float((sub[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
-        print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f per req" % (a, sel, p2, rem, p1, fb))
+        fb = float((sub[:, 3] & np.uint64(0xFFFF)).sum()) / nreq
+        nt = float(((sub[:, 3] >> np.uint64(16)) & np.uint64(0xFFFF)).sum()) / nreq
+        print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f near-tie %.4f per req"
+              % (a, sel, p2, rem, p1, fb, nt))
 if os.environ.get("DUMP"):
     os.makedirs("gpurun_out", exist_ok=True)
     np.savez(os.environ["DUMP"], cycles=cyc, counters=ctr, chains=g.chains.astype(np.int64),
