@@ -1202,6 +1202,9 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       }
       return best;
     }
+#ifdef MC_PHASE_TIMERS3
+    CC.t_unpin += 1ull << 16;  // near-tie verifications (bits 16..31)
+#endif
     ENSURE_EXTREMES();
     if (mine) {  // near-ties: exact utilities, ids for exact ties
       best.t = d_tc(C, i1);
