@@ -1006,6 +1006,46 @@ __device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* ta
   return best;
 }
 
+// Pass 1 of the α > 0 selection (cold: only when the bound cache was invalidated, ~7 % of
+// requests), out of line to keep it out of the hot loop's instruction footprint: exact t
+// bounds and fp32 eff bounds over every non-root node (R1; holes excluded).
+struct Bounds32 {
+  uint32_t tmin, tmax;
+  float lo, hi;
+};
+__device__ __noinline__ Bounds32 bounds_pass(const DenseRec* sd, const DenseRec* tail, uint32_t cnt, uint32_t S) {
+  uint32_t tmn[kUnroll], tmx[kUnroll];
+  float lo[kUnroll], hi[kUnroll];
+#pragma unroll
+  for (int q = 0; q < kUnroll; q++) {
+    tmn[q] = 0xFFFFFFFFu; tmx[q] = 0; lo[q] = __int_as_float(0x7F800000); hi[q] = 0.0f;
+  }
+  auto f = [&](int q, uint32_t, uint32_t tc, float e) {
+    const uint32_t t = tc & T_MASK;
+    tmn[q] = min(tmn[q], t);
+    tmx[q] = max(tmx[q], tc == HOLE_TC ? 0u : t);
+    lo[q] = fminf(lo[q], e);
+    hi[q] = fmaxf(hi[q], e);
+  };
+  const uint32_t ns = min(cnt, S);
+  scan_block(sd, 0, ns, f);
+  if (cnt > ns) scan_block(tail, ns, cnt, f);
+  Bounds32 r;
+  r.tmin = tmn[0]; r.tmax = tmx[0]; r.lo = lo[0]; r.hi = hi[0];
+#pragma unroll
+  for (int q = 1; q < kUnroll; q++) {
+    r.tmin = min(r.tmin, tmn[q]); r.tmax = max(r.tmax, tmx[q]); r.lo = fminf(r.lo, lo[q]); r.hi = fmaxf(r.hi, hi[q]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    r.tmin = min(r.tmin, __shfl_xor_sync(FULL, r.tmin, o));
+    r.tmax = max(r.tmax, __shfl_xor_sync(FULL, r.tmax, o));
+    r.lo = fminf(r.lo, __shfl_xor_sync(FULL, r.lo, o));
+    r.hi = fmaxf(r.hi, __shfl_xor_sync(FULL, r.hi, o));
+  }
+  return r;
+}
+
 // α = 0 with the oldest t shared by several candidates: the one with the smallest id.
 __device__ __noinline__ uint32_t lru_tiebreak(const DenseRec* sd, const DenseRec* tail, const uint32_t* ids,
                                               uint32_t cnt, uint32_t S, uint32_t t) {
@@ -1104,36 +1144,12 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   if (C.bc_valid & 1u) {
     tmin = C.bc_tmin; tmax = C.bc_tmax; lo32 = C.bc_lo; hi32 = C.bc_hi;
   } else {
-  uint32_t tmn[kUnroll], tmx[kUnroll];
-  float lo[kUnroll], hi[kUnroll];
-#pragma unroll
-  for (int q = 0; q < kUnroll; q++) {
-    tmn[q] = 0xFFFFFFFFu; tmx[q] = 0; lo[q] = __int_as_float(0x7F800000); hi[q] = 0.0f;
-  }
-  scan_dense(C, cnt, [&](int q, uint32_t, uint32_t tc, float e) {
-    const uint32_t t = tc & T_MASK;
-    tmn[q] = min(tmn[q], t);
-    tmx[q] = max(tmx[q], tc == HOLE_TC ? 0u : t);
-    lo[q] = fminf(lo[q], e);
-    hi[q] = fmaxf(hi[q], e);
-  });
-  tmin = tmn[0]; tmax = tmx[0];
-  lo32 = lo[0]; hi32 = hi[0];
-#pragma unroll
-  for (int q = 1; q < kUnroll; q++) {
-    tmin = min(tmin, tmn[q]); tmax = max(tmax, tmx[q]); lo32 = fminf(lo32, lo[q]); hi32 = fmaxf(hi32, hi[q]);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    tmin = min(tmin, __shfl_xor_sync(FULL, tmin, o));
-    tmax = max(tmax, __shfl_xor_sync(FULL, tmax, o));
-    lo32 = fminf(lo32, __shfl_xor_sync(FULL, lo32, o));
-    hi32 = fmaxf(hi32, __shfl_xor_sync(FULL, hi32, o));
-  }
-  // the exact fp64 extremes are recovered only when a victim's exact utility is needed
-  Cw.bc_valid = 1; Cw.bc_tmin = tmin; Cw.bc_tmax = tmax; Cw.bc_lo = lo32; Cw.bc_hi = hi32;
+    const Bounds32 bp = bounds_pass(C.sd, C.w.tail(), cnt, C.S);
+    tmin = bp.tmin; tmax = bp.tmax; lo32 = bp.lo; hi32 = bp.hi;
+    // the exact fp64 extremes are recovered only when a victim's exact utility is needed
+    Cw.bc_valid = 1; Cw.bc_tmin = tmin; Cw.bc_tmax = tmax; Cw.bc_lo = lo32; Cw.bc_hi = hi32;
 #ifdef MC_PHASE_TIMERS3
-  CC.t_unpin += 1ull << 32;  // count full bound passes (high half)
+    CC.t_unpin += 1ull << 32;  // count full bound passes (high half)
 #endif
   }
   b.tmin = tmin;
