@@ -905,7 +905,7 @@ __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, 
   if (a == b) return cmp;  // same pool range: identical tokens
   const uint32_t lane = lane_id();
 #ifndef MC_MATCH_BLOCKS
-#define MC_MATCH_BLOCKS 4
+#define MC_MATCH_BLOCKS 8
 #endif
   constexpr int kB = MC_MATCH_BLOCKS;  // 32-token blocks compared per round trip
   for (uint32_t base = 0; base < cmp; base += 32 * kB) {
