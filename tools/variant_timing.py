@@ -19,7 +19,10 @@ for it in range(6):
     out["hit_sum"].zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    g.run(out=out, **({'n_workers': int(os.environ['NW'])} if os.environ.get('NW') else {}))
+    kw = {'n_workers': int(os.environ['NW'])} if os.environ.get('NW') else {}
+    if os.environ.get('SMEMN'):
+        kw['smem_nodes'] = int(os.environ['SMEMN'])
+    g.run(out=out, **kw)
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
