@@ -15,6 +15,8 @@ Parity status of each function:
                                                           flat-list brute force, independent LRU,
                                                           OPT bound, invariants
   run_chains (α-grid over segments)                     pinned: α=0 segment replay == live pass
+  counters (d.3 algorithmic bytes)                       pinned: the flat-list simulator's own
+                                                          counts (tests/flatlist.py) + S1 by hand
   live_pass (segment snapshots)                          pinned: as Oracle.run + dump round-trip
 """
 from __future__ import annotations
@@ -332,7 +334,8 @@ def live_tune(trace, variant, alphas: Sequence[float], multiplier: int = 10, n_t
     info["alpha_star"] = a_star
     info["grid_hit_sums"] = [int(x) for x in hs]
     if b_end < R:
-        o2 = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, a_star, _chunk(variant))
+        o2 = Oracle(trace, variant.model, variant.capacity_bytes, variant.capacity_nodes, a_star, _chunk(variant),
+                    _block(variant))
         o2.load(*end_snap)
         h, f, _ = o2.run(b_end + 1, R - b_end)
         hits[b_end:], flops[b_end:] = h, f

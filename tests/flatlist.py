@@ -68,11 +68,17 @@ class FlatCache:
         self.E: Dict[int, Entry] = {}
         self.next_id = 1
         self.log: List[Tuple[int, int, int, float]] = []
+        # SURVEY.md §8(d) d.3 counters, derived here from the brute-force relations:
+        # [Σ c_r = min(m+1, n), Σ v_r = |P| + 1, Σ_j N_j = live entries at eviction j,
+        #  Σ w_r = records written (touch 1, split 2, gain 1, leaf 1, timestamp-only 1,
+        #  leaf removal 1, absorption 2)]
+        self.ctr = [0, 0, 0, 0]
 
     def clone(self) -> "FlatCache":
         c = copy.copy(self)
         c.E = {k: Entry(e.path, e.has_ssm, e.t, e.id) for k, e in self.E.items()}
         c.log = list(self.log)
+        c.ctr = list(self.ctr)
         return c
 
     # ---- brute-force relations ----
@@ -133,6 +139,8 @@ class FlatCache:
             ext = [e for e in self.E.values() if len(e.path) > m and e.path[:m] == S[:m]]
             partial = min(ext, key=lambda e: len(e.path))
         P = full + ([partial] if partial else [])
+        self.ctr[0] += min(m + 1, n)
+        self.ctr[1] += len(P) + 1
         # speculative insertion with the c.3 #8/#9 readings
         m_in = min(m, L_in)
         q = 0
@@ -174,6 +182,7 @@ class FlatCache:
         d_nodes = len(splits) + (1 if leaf else 0)
         if hit is not None:
             hit.t = r
+            self.ctr[3] += 1
         pinned_bytes = sum(self.bytes(e) for e in P)
         bypass = (pinned_bytes + d_bytes > self.cap_bytes or
                   (self.cap_nodes and len(P) + d_nodes > self.cap_nodes))
@@ -186,19 +195,28 @@ class FlatCache:
                 victim, u = self._choose(cands, chooser, r)
                 kind = 0 if self.n_children(victim) == 0 else 1
                 self.log.append((r, victim.id, kind, u))
+                self.ctr[2] += len(self.E)
+                self.ctr[3] += 1 + kind
                 del self.E[victim.id]
             for x, stateful in splits:
                 self.E[self.next_id] = Entry(S[:x], stateful, r, self.next_id)
                 self.next_id += 1
+                self.ctr[3] += 2  # the new upper entry and the lower one's shortened edge
             if p_gain is not None:
                 p_gain.has_ssm, p_gain.t = True, r
+                self.ctr[3] += 1
             if n_gain is not None:
                 n_gain.has_ssm, n_gain.t = True, r
+                self.ctr[3] += 1
             if leaf:
                 self.E[self.next_id] = Entry(S, True, r, self.next_id)
                 self.next_id += 1
+                self.ctr[3] += 1
             else:
-                self.at(S, n).t = r
+                fin = self.at(S, n)
+                if not m_mid and n_gain is None and fin is not p_gain:
+                    self.ctr[3] += 1  # timestamp-only write of the existing final entry
+                fin.t = r
         return reuse, F(reuse, self.m), int(bool(bypass))
 
     def _choose(self, cands, chooser, r):
@@ -311,6 +329,7 @@ class FlatBlocks:
         self.E: Dict[int, Entry] = {}
         self.next_id = 1
         self.log: List[Tuple[int, int, int, float]] = []
+        self.ctr = [0, 0, 0, 0]  # d.3 counters, as FlatCache.ctr at block granularity
 
     def bb(self) -> int:
         return KVT(self.m) * self.x + SSMB(self.m)
@@ -336,6 +355,9 @@ class FlatBlocks:
         path = [self.cached(S[:(j + 1) * x]) for j in range(mb)]
         for e in path:
             e.t = r
+        self.ctr[0] += mb * x
+        self.ctr[1] += mb + 1
+        self.ctr[3] += mb
         bb = self.bb()
         n_new = nb - mb
         bypass = (mb + n_new) * bb > self.cap_bytes or bool(self.cap_nodes and nb > self.cap_nodes)
@@ -349,10 +371,13 @@ class FlatBlocks:
                 v = min(cands, key=lambda e: (e.t, e.id))
                 u = 0.5 if tmax == tmin else float(v.t - tmin) / float(tmax - tmin)
                 self.log.append((r, v.id, 0, u))
+                self.ctr[2] += len(self.E)
+                self.ctr[3] += 1
                 del self.E[v.id]
             for j in range(mb, nb):
                 self.E[self.next_id] = Entry(S[:(j + 1) * x], True, r, self.next_id)
                 self.next_id += 1
+                self.ctr[3] += 1
         return reuse, F(reuse, self.m), int(bool(bypass))
 
     def dump(self):

@@ -31,13 +31,14 @@ def _cap(seed):
     return (3 + seed % 3) * SSMB, 3 + seed % 5
 
 
-def _oracle_run(tr, model, capb, capn, a):
+def _oracle_run(tr, model, capb, capn, a, with_ctr=False):
     o = O.Oracle(tr, model, capb, capn, a)
     h, f, b = o.run(1, tr.n_requests)
     lg = o.log()
     d, _ = o.dump()
+    ctr = o.counters()
     o.close()
-    return h, f, b, lg, d
+    return (h, f, b, lg, d, ctr) if with_ctr else (h, f, b, lg, d)
 
 
 @pytest.mark.parametrize("block", range(10))
@@ -48,7 +49,7 @@ def test_flatlist_equivalence(block):
         model = tg.MODEL_7B if seed % 2 else tg.MODEL_TOY
         capb, capn = _cap(seed)
         a = GRID[seed % len(GRID)]
-        h, f, b, lg, d = _oracle_run(tr, model, capb, capn, a)
+        h, f, b, lg, d, ctr = _oracle_run(tr, model, capb, capn, a, with_ctr=True)
         res, fc = FL.replay(tr, model, capb, capn, a)
         assert [int(x) for x in h] == [x[0] for x in res], seed
         assert [int(x) for x in f] == [x[1] for x in res], seed
@@ -60,6 +61,25 @@ def test_flatlist_equivalence(block):
         dd = [(int(x["id"]), int(x["parent_id"]), int(x["d_start"]), int(x["d_end"]), int(x["has_ssm"]),
                int(x["t_last"])) for x in d]
         assert dd == fc.dump(), seed
+        # the d.3 algorithmic-byte counters (numerator of roofline.frac), derived
+        # independently from the brute-force relations
+        assert [int(x) for x in ctr] == fc.ctr, (seed, ctr, fc.ctr)
+
+
+def test_counters_pin_closed_form():
+    """Hand-derived d.3 counters of worked example S1, c_r = min(m+1, n),
+    v_r = |P| + 1, w_r = records written: r1 into an empty cache has m = 0 (c = 1), visits
+    only the root (v = 1) and writes its leaf (w = 1); r2 matches 16 of 32 tokens inside
+    r1's leaf (c = 17, P = {leaf}: v = 2), splits it at 16 (w = 2) and adds its leaf (w = 1);
+    r3 walks the stateful 16-token node and stops at its boundary (c = 17, v = 2), touches
+    the hit (w = 1) and adds its leaf (w = 1).  No evictions (unlimited capacity)."""
+    P = list(range(100, 116))
+    a, b, c = [200 + i for i in range(8)], [300 + i for i in range(8)], [400 + i for i in range(8)]
+    x, y, z = [500 + i for i in range(8)], [600 + i for i in range(8)], [700 + i for i in range(8)]
+    tr = tg.from_sequences([(P + a, x), (P + b, y), (P + c, z)])
+    h, f, bb, lg, d, ctr = _oracle_run(tr, tg.MODEL_7B, tg.UNLIMITED_BYTES, 0, 0.0, with_ctr=True)
+    assert [int(v) for v in h] == [0, 0, 16]
+    assert [int(v) for v in ctr] == [1 + 17 + 17, 1 + 2 + 2, 0, 1 + 3 + 2]
 
 
 def test_lru_equivalence_alpha0():

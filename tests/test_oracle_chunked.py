@@ -46,6 +46,7 @@ def test_flatlist_equivalence_chunked(chunk):
         h, f, b = o.run(1, tr.n_requests)
         res, fc = FL.replay(tr, tg.MODEL_7B, tg.UNLIMITED_BYTES, capn, a, chunk=chunk)
         assert [int(x) for x in h] == [x[0] for x in res], (chunk, seed)
+        assert [int(x) for x in o.counters()] == fc.ctr, (chunk, seed)
         lg = o.log()
         assert [(int(x["req"]), int(x["node_id"]), int(x["kind"])) for x in lg] == \
             [(r, i, k) for r, i, k, _ in fc.log], (chunk, seed)

@@ -49,3 +49,17 @@ def test_no_eviction_keeps_alpha0():
     v = tg.Variant(tg.MODEL_7B, tg.UNLIMITED_BYTES)
     h, f, info = O.live_tune(tr, v, [0.0, 1.0])
     assert info["r_first_evict"] == 0 and info["alpha_star"] == 0.0
+
+
+def test_vllm_variant_keeps_its_policy_after_adoption():
+    """Regression: the adopt phase replays with the variant's own policy.  A vLLM+ chain
+    ignores α (reading V8), so every grid entry ties, α* = 0, and the whole tuned run must
+    equal the plain vLLM+ live pass -- including the requests after the window."""
+    tr, _ = _small()
+    v = tg.Variant(tg.MODEL_7B, 4 * tg.GB, 0, 0, 32)
+    h, f, info = O.live_tune(tr, v, [0.0, 1.0, 64.0])
+    assert info["window"] is not None and info["window"][1] < tr.n_requests
+    assert len(set(info["grid_hit_sums"])) == 1 and info["alpha_star"] == 0.0
+    o = O.Oracle(tr, v.model, v.capacity_bytes, 0, 0.0, block=32)
+    h0, f0, _ = o.run(1, tr.n_requests)
+    assert np.array_equal(h, h0) and np.array_equal(f, f0)

@@ -30,13 +30,14 @@ def _bb(model, x):
     return FL.KVT(model) * x + FL.SSMB(model)
 
 
-def _run(tr, model, capb, capn, x):
+def _run(tr, model, capb, capn, x, with_ctr=False):
     o = O.Oracle(tr, model, capb, capn, 0.0, block=x)
     h, f, b = o.run(1, tr.n_requests)
     lg, (d, nid) = o.log(), o.dump()
     tot = o.total()
+    ctr = o.counters()
     o.close()
-    return h, f, b, lg, d, tot
+    return (h, f, b, lg, d, tot, ctr) if with_ctr else (h, f, b, lg, d, tot)
 
 
 def _cap(seed, model, x):
@@ -57,7 +58,7 @@ def test_flat_blocks_equivalence(part):
         model = M7 if seed % 2 else tg.MODEL_TOY
         x = 1 + seed % 8
         capb, capn = _cap(seed, model, x)
-        h, f, b, lg, d, _ = _run(tr, model, capb, capn, x)
+        h, f, b, lg, d, _, ctr = _run(tr, model, capb, capn, x, with_ctr=True)
         res, fc = FL.replay_blocks(tr, model, capb, capn, x)
         assert [int(v) for v in h] == [r[0] for r in res], seed
         assert [int(v) for v in f] == [r[1] for r in res], seed
@@ -67,6 +68,7 @@ def test_flat_blocks_equivalence(part):
         dd = [(int(e["id"]), int(e["parent_id"]), int(e["d_start"]), int(e["d_end"]), int(e["has_ssm"]),
                int(e["t_last"])) for e in d]
         assert dd == fc.dump(), seed
+        assert [int(v) for v in ctr] == fc.ctr, (seed, ctr, fc.ctr)  # d.3 counters
 
 
 def test_fig2b_17_4_GB_one_10k_sequence_block16():
