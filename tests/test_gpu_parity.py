@@ -285,13 +285,16 @@ def test_chain_subsets_and_order_do_not_matter():
 
 
 def _full_grid_parity(cfg, log_chains=()):
-    """All chains of BASELINE config `cfg` at full size, in the bench launch configuration,
-    against the oracle (live-pass snapshots, every request of every chain, hit sums, α*)."""
+    """All chains of BASELINE config `cfg` at full size, in the bench launch configuration
+    (eviction logs OFF: the branch bench.py times), against the oracle (live-pass snapshots,
+    every request of every chain, d.3 counters, hit sums, α*).  Then a second replay call
+    with eviction logs on the `log_chains` subset: logs equal the oracle's bitwise and
+    turning logs on changes no output."""
     import os
     w = tg.workload(cfg)
     tr = w.trace
     g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
-    out = g.run(counters=True, log_cap=16384 if log_chains else 0)
+    out = g.run(counters=True)
     g.ctx.check()
     hit, fl, by = (out[x].cpu().numpy() for x in ("hit", "flops", "bypass"))
     ctr = out["counters"].cpu().numpy()
@@ -312,17 +315,26 @@ def _full_grid_parity(cfg, log_chains=()):
         assert np.array_equal(fl[v, ai, sl], f.astype(np.int64)), cid
         assert np.array_equal(by[v, ai, sl], b.astype(np.uint8)), cid
         assert np.array_equal(ctr[cid], c.astype(np.int64)), cid
-    for cid in log_chains:
-        v, ai, si = cid // (na * ns), (cid // ns) % na, cid % ns
-        first, n, k = segs[si]
-        _, _, _, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[v][k])
-        glog, gn = g.ctx.read_log(out, cid)
-        _assert_logs_equal(glog, gn, lg, f"cfg{cfg} chain {cid}")
     a_star = g.select(out)
     for v in range(len(w.variants)):
         sums = [sum(int(res[(v * na + ai) * ns + si][0].sum()) for si in range(ns)) for ai in range(na)]
         assert [int(x) for x in g.hit_sums[v]] == sums
         assert a_star[v] == O.select_alpha(w.alphas, sums)
+    if log_chains:
+        out2 = g.ctx.alloc_outputs(na, log_cap=16384, counters=True)
+        g.ctx.replay(w.alphas, chains=list(log_chains), out=out2)
+        g.ctx.check()
+        h2 = out2["hit"].cpu().numpy()
+        c2 = out2["counters"].cpu().numpy()
+        for cid in log_chains:
+            v, ai, si = cid // (na * ns), (cid // ns) % na, cid % ns
+            first, n, k = segs[si]
+            sl = slice(first - 1, first - 1 + n)
+            assert np.array_equal(h2[v, ai, sl], hit[v, ai, sl]), cid
+            assert np.array_equal(c2[cid], ctr[cid]), cid
+            _, _, _, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[v][k])
+            glog, gn = g.ctx.read_log(out2, cid)
+            _assert_logs_equal(glog, gn, lg, f"cfg{cfg} chain {cid}")
     return g, out
 
 
@@ -343,28 +355,57 @@ def test_full_config4_swebench():
 
 def test_full_config5_sampled():
     """configs[4]: 200k requests x 15 cache variants (1:2/1:4/1:8 x 60-140 GB) x 16 α x 16
-    segments = 3,840 chains on the device; sampled snapshots/chains vs the oracle, and
-    invariants on every chain."""
+    segments = 3,840 chains on the device (logs off, the bench launch).  Against the oracle:
+    live passes and snapshots 0-2 of every variant, and ONE FULL SEGMENT (12,500 requests)
+    for all 15 variants x 16 α = 240 chains (hits, FLOPs, bypass, d.3 counters); eviction
+    logs of 6 of those chains from a second, logged call.  Every chain: hit <= L_in and
+    α = 0 replays == the device live pass.  (All 3,840 chains against the oracle:
+    tools/parity_full.py --config 5, summary in profiles/r02_parity_cfg5.json.)"""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
     w = tg.workload(5)
     tr = w.trace
+    nv, na = len(w.variants), len(w.alphas)
     g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
-    out = g.run()
+    out = g.run(counters=True)
     g.ctx.check()
-    hit = out["hit"].cpu().numpy()
+    hit, fl, by = (out[x].cpu().numpy() for x in ("hit", "flops", "bypass"))
+    ctr = out["counters"].cpu().numpy()
     live = g.live[0].cpu().numpy()
     assert (hit <= tr.lin[None, None, :]).all()
-    for v in range(len(w.variants)):
+    for v in range(nv):
         assert np.array_equal(hit[v, 0], live[v])          # α = 0 segment replays == live pass
-    W = g.window
-    for v in (0, 7, 14):
-        snaps, h_live, *_ = O.live_pass(tr, w.variants[v], W, upto=2 * W)
-        assert np.array_equal(live[v][: 2 * W], h_live)
-        gs, gn = g.ctx.get_snapshot(v, 1)
-        assert gn == snaps[1][1] and np.array_equal(GU.canon(gs), GU.canon(snaps[1][0])), v
-        for ai in (1, 8, 15):
-            first, n, _ = g.segs[1]
-            h, f, b, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, snaps[1])
-            assert np.array_equal(hit[v, ai, first - 1:first - 1 + n], h), (v, ai)
+    W, ns = g.window, len(g.segs)
+    with ThreadPoolExecutor(max_workers=min(nv, os.cpu_count() or 1)) as ex:
+        lp = list(ex.map(lambda v: O.live_pass(tr, v, W, upto=2 * W), w.variants))
+    for v in range(nv):
+        snaps, h_live = lp[v][0], lp[v][1]
+        assert np.array_equal(live[v][: 2 * W], h_live), v
+        for k in (1, 2):
+            gs, gn = g.ctx.get_snapshot(v, k)
+            assert gn == snaps[k][1] and np.array_equal(GU.canon(gs), GU.canon(snaps[k][0])), (v, k)
+    si = 1
+    first, n, k = g.segs[si]
+    flat = [lp[v][0][k] for v in range(nv)]
+    chains = [(v, w.alphas[ai], first, n, v) for v in range(nv) for ai in range(na)]
+    oh, of, ob, _, octr = O.run_chains(tr, w.variants, chains, flat, n_threads=os.cpu_count() or 1)
+    sl = slice(first - 1, first - 1 + n)
+    for i, (v, alpha, *_rest) in enumerate(chains):
+        ai = i % na
+        cid = (v * na + ai) * ns + si
+        assert np.array_equal(hit[v, ai, sl], oh[i]), (v, ai)
+        assert np.array_equal(fl[v, ai, sl], of[i].astype(np.int64)), (v, ai)
+        assert np.array_equal(by[v, ai, sl], ob[i].astype(np.uint8)), (v, ai)
+        assert np.array_equal(ctr[cid], octr[i].astype(np.int64)), (v, ai)
+    logged = [(0, 5), (4, 15), (7, 1), (9, 9), (12, 12), (14, 3)]
+    ids = [(v * na + ai) * ns + si for v, ai in logged]
+    out2 = g.ctx.alloc_outputs(na, log_cap=1 << 15)
+    g.ctx.replay(w.alphas, chains=ids, out=out2)
+    g.ctx.check()
+    for (v, ai), cid in zip(logged, ids):
+        _, _, _, lg = GU.oracle_chain_log(tr, w.variants[v], w.alphas[ai], first, n, flat[v])
+        glog, gn = g.ctx.read_log(out2, cid)
+        _assert_logs_equal(glog, gn, lg, f"cfg5 v{v} a{ai}")
     a_star = g.select(out)
     assert len(a_star) == 15 and all(a in w.alphas for a in a_star)
 
@@ -552,3 +593,36 @@ def test_dense_positions_beyond_half_the_node_table():
     w.variants = [_vllm(tg.MODEL_7B, 120 * tg.GB, 0, 16)]
     w.alphas = (0.0,)
     _compare_grid(w)
+
+
+# ---------------------------------------------------------------- fp32 filter edge cases
+def test_adversarial_filter_near_ties():
+    """The kernel's fp32 filter-and-verify argmin on built edge
+    cases (tests/adversarial.py): Δe32 = 0 and 1 ulp, top-2 exact utilities within 4 ulps,
+    α = 64 (up to 1e300) with a tiny Δe, exact (u, t) ties.  Snapshots are uploaded through
+    mc_set_snapshots; every eviction of every (case, α) chain -- logs OFF first (the bench
+    branch: hits, FLOPs, bypass, counters), then logs ON -- must equal the oracle's,
+    utilities bit for bit."""
+    import adversarial as A
+    n_ev = 0
+    for c in A.make_cases(range(240)):
+        ctx = M.Context([c.variant], max_nodes=128)
+        ctx.upload_trace(c.trace.tokens, c.trace.off, c.trace.lin, c.trace.lout)
+        ctx.set_snapshots(0, [c.snapshot])
+        ctx.set_segments([(c.first, c.n, 0)])
+        o0 = ctx.replay(c.alphas, counters=True)
+        o1 = ctx.replay(c.alphas, log_cap=16, counters=True)
+        ctx.check()
+        sl = slice(c.first - 1, c.first - 1 + c.n)
+        for ai, a in enumerate(c.alphas):
+            h, f, b, lg = GU.oracle_chain_log(c.trace, c.variant, a, c.first, c.n, c.snapshot)
+            for o in (o0, o1):
+                assert np.array_equal(o["hit"].cpu().numpy()[0, ai, sl], h), a
+                assert np.array_equal(o["flops"].cpu().numpy()[0, ai, sl], f.astype(np.int64)), a
+                assert np.array_equal(o["bypass"].cpu().numpy()[0, ai, sl], b.astype(np.uint8)), a
+            assert torch.equal(o0["counters"], o1["counters"])
+            glog, gn = ctx.read_log(o1, ai)
+            _assert_logs_equal(glog, gn, lg, f"case {c.tmode} alpha {a!r}")
+            n_ev += gn
+        ctx.close()
+    assert n_ev > 5000
