@@ -167,12 +167,16 @@ mc_status mc_snapshot_count(const mc_ctx* ctx, uint32_t variant, uint32_t* n_out
 mc_status mc_get_snapshot(mc_ctx* ctx, uint32_t variant, uint32_t k, mc_snap_node* h_out, uint64_t cap,
                           uint64_t* n_out, uint32_t* next_id);
 
-/* Replay windows.  Chain c = ((variant * n_alpha) + alpha_idx) * n_segs + seg. */
+/* Replay windows.  Chain c = ((variant * n_alpha) + alpha_idx) * n_segs + seg.
+ * Each window must hold >= 1 request inside the trace (MC_EINVAL otherwise). */
 mc_status mc_set_segments(mc_ctx* ctx, const mc_segment* h_segs, uint32_t n_segs);
 
 /* Workspaces (d_workspace of mc_replay / mc_live_pass) must be ZERO-INITIALISED
  * by the caller when first allocated; they may then be reused across calls of
- * the same context without clearing.
+ * the same context without clearing (the per-worker slices sit at a fixed offset,
+ * whatever the chain count of a call).  One workspace serves one call at a time;
+ * calls that may overlap (other streams) need their own workspaces -- each call's
+ * α grid and chain list travel in its workspace.
  * Workspace bytes for `n_workers` concurrent chains (one warp each; 0 = the
  * default: every SM filled at the kernel's occupancy) and up to n_chains chain
  * ids per mc_replay call (0 = every chain of n_alpha α values). */
@@ -205,8 +209,15 @@ typedef struct {
                                memory (0 = auto: fill the SM at the target occupancy) */
 } mc_replay_args;
 
-/* Run the chains (asynchronous on `stream`).  Each chain loads its snapshot,
- * replays its window at its α and writes per-request outputs and its hit sum. */
+/* The α-grid replay (§4.2 "Managing the balance": replay the
+ * bootstrap requests from the tree snapshot for every α of the grid; here one chain =
+ * (variant, α, segment)).  Asynchronous on `stream`.  Each chain loads its segment's
+ * snapshot and replays its window request by request -- hybrid lookup + speculative
+ * insertion, admission, Eq. 2 eviction
+ * until the request fits -- writing d_hit / d_flops / d_bypass
+ * per request and adding its Σ hits to d_hit_sum[variant][alpha].  Argument errors
+ * (NaN / negative / infinite α, bad chain ids, workspace too small, missing
+ * snapshots) return synchronously; device-side failures go to mc_check. */
 mc_status mc_replay(mc_ctx* ctx, const mc_replay_args* args, void* stream);
 
 /* Copy one chain's eviction log of an mc_replay call to the host (SURVEY.md §8(b)

@@ -293,15 +293,20 @@ struct mc_ctx {
   std::vector<mc_segment> segs;
   mc_segment* d_segs = nullptr;
   uint32_t* d_status = nullptr;
-  double* d_alphas = nullptr;  // small device buffer (64 entries)
   uint32_t* d_points = nullptr;  // live-pass snapshot points + first-eviction outputs
-  uint32_t alpha_cap = 0;
+  uint32_t alpha_cap = 0;        // α values per mc_replay call (they travel in the workspace header)
   char* img_scratch = nullptr;   // image_kernel workspace slices (zeroed once, reused: generation tags)
   uint64_t img_scratch_bytes = 0;
 };
 
 namespace {
-constexpr uint64_t kCtrl = 4096;  // workspace control header (queue counter, ...)
+// Workspace layout: control header (kCtrl bytes: queue counters at 0 and 64, this call's
+// α grid at kAlphaOff, live-pass snapshot views at 256) | worker slices at the FIXED offset
+// kCtrl (so a workspace reused with a different chain count keeps every slice -- and its
+// child-index generation header -- in place) | the call's chain ids at the end.
+constexpr uint64_t kCtrl = 4096;
+constexpr uint64_t kAlphaOff = 2048;  // up to 256 doubles
+uint64_t ids_bytes(uint64_t n_chains) { return (4ull * n_chains + 255) & ~255ull; }
 
 DevModel make_model(const mc_model& m) {
   // Appendix A tab:flops_breakdown summed over layers, and PAPER:814.
@@ -485,11 +490,10 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     c->dvh.push_back(d);
   }
   c->snaps.resize(n_var);
-  c->alpha_cap = 256;
+  c->alpha_cap = (uint32_t)((kCtrl - kAlphaOff) / sizeof(double));  // 256
   if (cudaMalloc(&c->d_var, sizeof(DevVariant) * n_var) != cudaSuccess ||
       cudaMalloc(&c->d_stores, sizeof(DevSnapStore) * n_var) != cudaSuccess ||
-      cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess ||
-      cudaMalloc(&c->d_alphas, sizeof(double) * c->alpha_cap) != cudaSuccess) {
+      cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess) {
     mc_destroy(c);
     return fail(MC_ENOMEM, "mc_create: device allocation failed");
   }
@@ -511,7 +515,6 @@ void mc_destroy(mc_ctx* c) {
   cudaFree(c->d_stores);
   cudaFree(c->d_segs);
   cudaFree(c->d_status);
-  cudaFree(c->d_alphas);
   cudaFree(c->d_points);
   delete c;
 }
@@ -611,8 +614,7 @@ mc_status mc_workspace_size(const mc_ctx* c, uint32_t n_workers, uint32_t n_alph
   if (!c || !bytes) return fail(MC_EINVAL, "mc_workspace_size: null argument");
   if (n_workers == 0) n_workers = default_workers(c);
   if (n_chains == 0) n_chains = (uint32_t)(c->hv.size() * std::max(1u, n_alpha) * std::max<size_t>(1, c->segs.size()));
-  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
-  *bytes = head + (uint64_t)n_workers * ws_bytes_per_worker(c->ncap, c->hcap);
+  *bytes = kCtrl + (uint64_t)n_workers * ws_bytes_per_worker(c->ncap, c->hcap) + ids_bytes(n_chains);
   return MC_OK;
 }
 
@@ -620,8 +622,8 @@ mc_status mc_workspace_workers(const mc_ctx* c, uint64_t bytes, uint32_t n_alpha
                                uint32_t* n_workers) {
   if (!c || !n_workers) return fail(MC_EINVAL, "mc_workspace_workers: null argument");
   if (n_chains == 0) n_chains = (uint32_t)(c->hv.size() * std::max(1u, n_alpha) * std::max<size_t>(1, c->segs.size()));
-  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
-  *n_workers = bytes <= head ? 0 : (uint32_t)((bytes - head) / ws_bytes_per_worker(c->ncap, c->hcap));
+  const uint64_t fixed = kCtrl + ids_bytes(n_chains);
+  *n_workers = bytes <= fixed ? 0 : (uint32_t)((bytes - fixed) / ws_bytes_per_worker(c->ncap, c->hcap));
   return MC_OK;
 }
 
@@ -747,6 +749,7 @@ mc_status mc_set_segments(mc_ctx* c, const mc_segment* h_segs, uint32_t n_segs) 
   if (!c->tok) return fail(MC_ESTATE, "mc_set_segments before mc_set_trace");
   for (uint32_t i = 0; i < n_segs; i++) {
     const mc_segment& s = h_segs[i];
+    if (s.n_req == 0) return fail(MC_EINVAL, "segment " + std::to_string(i) + ": empty window (n_req == 0)");
     if (s.first_req < 1 || (uint64_t)s.first_req + s.n_req - 1 > c->n_req)
       return fail(MC_EINVAL, "segment " + std::to_string(i) + " outside the trace");
   }
@@ -787,17 +790,20 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
       if (vl == (pass == 1)) ids.push_back(id);
       if (pass == 0 && !vl) n_marconi++;
     }
-  const uint64_t head = kCtrl + ((4ull * n_chains + 255) & ~255ull);
+  const uint64_t fixed = kCtrl + ids_bytes(n_chains);
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
-  if (A->workspace_bytes < head + per) return fail(MC_ENOMEM, "workspace too small");
-  uint32_t workers = (uint32_t)((A->workspace_bytes - head) / per);
+  if (A->workspace_bytes < fixed + per) return fail(MC_ENOMEM, "workspace too small");
+  uint32_t workers = (uint32_t)((A->workspace_bytes - fixed) / per);
   if (A->n_workers) workers = std::min(workers, A->n_workers);
   workers = std::min(workers, n_chains);
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)A->d_workspace;
+  char* ids_at = ws + (A->workspace_bytes - ids_bytes(n_chains)) / 256 * 256;
+  // the α grid travels with the call (in its workspace), so concurrent calls on other
+  // streams with other workspaces never see each other's grid
   CU(cudaMemsetAsync(ws, 0, 256, st));
-  CU(cudaMemcpyAsync(ws + kCtrl, ids.data(), 4ull * n_chains, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(c->d_alphas, A->h_alphas, sizeof(double) * A->n_alpha, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(ws + kAlphaOff, A->h_alphas, sizeof(double) * A->n_alpha, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(ids_at, ids.data(), 4ull * n_chains, cudaMemcpyHostToDevice, st));
   KParams P;
   memset(&P, 0, sizeof(P));
   P.tok = c->tok;
@@ -810,14 +816,14 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   P.segs = c->d_segs;
   P.n_segs = ns;
   P.n_alpha = A->n_alpha;
-  P.alphas = c->d_alphas;
-  P.chains = (const uint32_t*)(ws + kCtrl);
+  P.alphas = (const double*)(ws + kAlphaOff);
+  P.chains = (const uint32_t*)ids_at;
   P.n_chains = n_chains;
   P.ncap = c->ncap;
   P.hcap = c->hcap;
   P.n_workers = workers;
   P.queue = (unsigned*)ws;
-  P.ws = ws + head;
+  P.ws = ws + kCtrl;
   P.ws_stride = per;
   P.hit = A->d_hit;
   P.flops = (unsigned long long*)A->d_flops;
@@ -840,7 +846,7 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   uint32_t first = 0;
   for (int g = 0; g < 2; g++) {
     if (groups[g] == 0) continue;
-    P.chains = (const uint32_t*)(ws + kCtrl) + first;
+    P.chains = (const uint32_t*)ids_at + first;
     P.n_chains = groups[g];
     P.queue = (unsigned*)ws + 16 * g;
     P.n_workers = std::min(workers, groups[g]);

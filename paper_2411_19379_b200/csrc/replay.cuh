@@ -1187,7 +1187,6 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
 #pragma unroll
   for (int o = 16; o; o >>= 1) kmin = fminf(kmin, __shfl_xor_sync(FULL, kmin, o));
   T3(t_evict);
-  if (kmin == INF) return best;  // no candidate
   // exact fp64 extremes (lazily, the fp64 values of the entries holding the fp32 extremes)
 #define ENSURE_EXTREMES()                                                                  \
   do {                                                                                     \
@@ -1197,6 +1196,13 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     }                                                                                      \
     b.emin = C.bc_elo; b.emax = C.bc_ehi;                                                  \
   } while (0)
+  // No finite filter key: either no candidate at all (exact_select then reports none) or
+  // an α so large that α/Δe32 or the key overflows fp32 (0 * inf = NaN keys never win the
+  // comparisons): the exact fp64 pass decides, as the oracle does for any finite α.
+  if (!(kmin < INF)) {
+    ENSURE_EXTREMES();
+    return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.K->alpha);
+  }
   // δ = 2^-19 (1 + α (1 + 4 emax/Δe32)); a zero fp32 range cannot resolve eff -> exact pass
   if (de32 == 0.0) ENSURE_EXTREMES();
   const bool exact_only = (de32 == 0.0) && (b.emax != b.emin);
