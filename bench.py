@@ -8,11 +8,18 @@ trace segments = 2,048 chains.  At N GPUs: N independent problems of that shape
 (trace seeds k = 0..N-1; weak scaling), the chains of every problem
 LPT-sharded across all ranks.  A step = replay of this rank's chains from their
 segment snapshots + one NCCL all-gather of per-(problem, α) hit sums + α*
-selection.  Why weak: a chain is sequential, and one
-problem's 2,048 chains already run concurrently on one B200, so a fixed chain
-list cannot get faster on more GPUs.
+selection.  Why weak by default: a chain is sequential, and
+one config-3 problem's 2,048 chains already run concurrently on one B200, so a
+fixed chain list of that size cannot get much faster on more GPUs.  `--scaling
+strong` shards ONE problem's chain list over the ranks instead (SURVEY.md d.4;
+config 5's 3,840 chains take two waves on one GPU).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3]
+                  [--scaling weak|strong]
+
+`--gpus N` without torchrun re-launches itself as N ranks (torch.distributed.run on
+127.0.0.1).  If fewer GPUs are visible than ranks, ranks share devices and exchange
+over gloo (flagged in the line's config: runnable, not a scaling number).
 
 Setup (untimed, reported): trace generation, H2D, the α = 0 device live pass
 that produces the 128 segment snapshots.  L2 is flushed (a 256 MiB write)
@@ -57,7 +64,28 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target wall time of the oracle sample")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: N independent problems at N GPUs (default); strong: ONE problem's chain list "
+                        "LPT-sharded over the N ranks (SURVEY.md d.4; the primary mode for config 5)")
     return p.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def respawn(args):
+    """`bench.py --gpus N` (N > 1) started without torchrun: re-launch itself as N ranks,
+    one process per GPU (torch.distributed.run, rendezvous on 127.0.0.1), and exit with
+    the ranks' status.  Rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def peaks():
@@ -195,7 +223,7 @@ def reference_arm(args, w, config):
     v = tot_n / tot_t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
             "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{len(chains)} chains of the first {k} segments per step"},
@@ -208,9 +236,10 @@ def reference_arm(args, w, config):
 # ----------------------------------------------------------------------------
 def main():
     args = parse()
+    respawn(args)
     import tracegen as tg
     rank, world, local = dist_env()
-    n_prob = max(1, world) if args.impl == "b200" else 1
+    n_prob = max(1, world) if (args.impl == "b200" and args.scaling == "weak") else 1
     t_gen = time.perf_counter()
     ws = [tg.workload(args.config, R=args.requests or None, problem=k) for k in range(n_prob)]
     if args.policy == "vllm":  # NEXT-2: the vLLM+ baseline on the same traces, block x cache-size sweep
@@ -228,7 +257,9 @@ def main():
     config = {"workload": f"config{args.config} {w.name}-shaped trace, {pol}{tr.n_requests} requests, "
                           f"{len(w.variants)} cache variant(s), {len(w.alphas)} alphas x {len(w.segments())} "
                           f"segments = {w.n_chains} chains" +
-                          (f"; x {n_prob} independent problems (one per GPU, weak scaling)" if n_prob > 1 else ""),
+                          (f"; x {n_prob} independent problems (one per GPU, weak scaling)" if n_prob > 1 else "") +
+                          (f"; one chain list sharded over {world} ranks (strong scaling)"
+                           if args.scaling == "strong" and world > 1 else ""),
               "requests": tr.n_requests, "tokens": tr.n_tokens, "alphas": len(w.alphas),
               "segments": len(w.segments()), "chains": w.n_chains * n_prob, "window": w.window,
               "problems": n_prob, "policy": args.policy,
@@ -240,12 +271,20 @@ def main():
 
     import torch
     import torch.distributed as dist
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
+    n_dev = torch.cuda.device_count()
+    # one process per GPU; if fewer GPUs are visible than ranks (e.g. a 1-GPU box asked for
+    # --gpus 2), ranks share devices round-robin and exchange over gloo (NCCL refuses two
+    # ranks on one device) -- a runnable but not a scaling measurement, flagged in config
+    shared = world > n_dev
+    dev = local % max(1, n_dev)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    if shared:
+        config["ranks_share_gpus"] = f"{world} ranks on {n_dev} visible GPU(s): exchange over gloo; not a scaling number"
     from paper_2411_19379_b200 import AlphaGrid
     from paper_2411_19379_b200.grid import gather_hit_sums
 
@@ -255,7 +294,7 @@ def main():
     t_setup = time.perf_counter()
     gs = []
     for k, wk in enumerate(ws):
-        g = AlphaGrid(wk.trace, wk.variants, wk.alphas, wk.n_segments, rank=rank, world=world, device=local)
+        g = AlphaGrid(wk.trace, wk.variants, wk.alphas, wk.n_segments, rank=rank, world=world, device=dev)
         g.setup()
         gs.append(g)
     torch.cuda.synchronize()
@@ -295,7 +334,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     clocks.start()
     time.sleep(0.3)
     step_ms, kern_ms = [], []
@@ -319,9 +358,9 @@ def main():
     clk = clocks.stop()
     for g in gs:
         g.ctx.check()
-    tot = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device="cpu" if shared else "cuda")
     if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)   # max over ranks (device-timed per rank)
     T_ms, K_ms = float(tot[0]), float(tot[1])
     value = all_reqs * args.steps / (T_ms / 1000.0)
 
@@ -347,7 +386,7 @@ def main():
     # e2e through the public API with host buffers (this rank's shards of every problem)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_measure(gs, ws, args, outs)
+        e2e = e2e_measure(gs, ws, args, outs, shared)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -357,9 +396,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": dict(config, parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one NCCL "
-                                                 f"all-gather of per-(problem, alpha) hit sums per step",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+            "config": dict(config, parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one "
+                                                 f"{'gloo' if shared else 'NCCL'} all-gather of per-(problem, alpha) "
+                                                 f"hit sums per step",
                            alpha_star=[a[0] for a in a_star],
                            setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -376,7 +416,7 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_measure(gs, ws, args, outs):
+def e2e_measure(gs, ws, args, outs, shared=False):
     """Same metric end to end through the C ABI from host buffers: per step, for every
     problem, H2D of the trace (tokens + requests, pinned) and of the segment snapshots,
     the replay of this rank's chains, D2H of the per-request hits and the hit sums."""
@@ -427,7 +467,7 @@ def e2e_measure(gs, ws, args, outs):
     dt = time.perf_counter() - t0
     import torch.distributed as dist
     if dist.is_initialized():
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t[0])
     return {"value": n_units * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

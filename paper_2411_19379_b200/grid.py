@@ -80,12 +80,13 @@ def gather_hit_sums(hs, world: int, group=None):
         g = torch.empty((world,) + tuple(hs.shape), dtype=hs.dtype, device=hs.device)
         dist.all_gather_into_tensor(g, hs.contiguous(), group=group)
         return g.sum(0)
-    parts = [torch.empty_like(hs) for _ in range(world)]
-    dist.all_gather(parts, hs.contiguous(), group=group)
-    tot = torch.zeros_like(hs)
+    h = hs.detach().cpu().contiguous()  # gloo: host tensors
+    parts = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(parts, h, group=group)
+    tot = torch.zeros_like(h)
     for p in parts:
         tot += p
-    return tot
+    return tot.to(hs.device)
 
 
 class AlphaGrid:
