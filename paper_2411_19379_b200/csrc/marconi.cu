@@ -60,6 +60,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
   const uint32_t lane = lane_id();
   const uint32_t worker = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (worker >= P.n_workers) return;
+  {  // the warp's snapshot-copy mbarrier and phase word (dense slots S + 12, S + 13)
+    char* sw = smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes;
+    const uint32_t S = P.smem_nodes - kSmemReserved;
+    if (lane == 0) {
+      mbar_init(reinterpret_cast<uint64_t*>(sw + 8ull * (S + 12)));
+      *reinterpret_cast<uint32_t*>(sw + 8ull * (S + 13)) = 0;
+    }
+    __syncwarp();
+  }
   for (;;) {
     uint32_t qi = 0;
     if (lane == 0) qi = atomicAdd(P.queue, 1u);
@@ -73,8 +82,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     const DevVariant V = P.var[v];
     const mc_segment seg = P.segs[s];
     Chain C;
-    // the warp's shared memory: dense slots [0, S - 12), the counters (32 B), the chain
-    // constants (64 B)
+    // the warp's shared memory: dense slots [0, S), the counters (32 B), the chain
+    // constants (64 B), the snapshot-copy mbarrier and its phase word
     char* sw = smem + (threadIdx.x >> 5) * 8ull * P.smem_nodes;
     const uint32_t S = P.smem_nodes - kSmemReserved;
     chain_init(C, P, worker, V, P.alphas[a], sw, S, reinterpret_cast<ChainConst*>(sw + 8ull * (S + 4)),
@@ -838,7 +847,7 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   uint32_t S = A->smem_nodes ? A->smem_nodes : c->smem_nodes;
   S = std::min<uint32_t>(S, c->ncap) & ~31u;
   if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
-  if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (12 slots hold the chain counters and constants)");
+  if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (14 slots hold the chain counters, constants and the copy mbarrier)");
   P.smem_nodes = S;
   // one launch per policy group, back to back on `st` (they share the worker slices);
   // each launch has its own queue word

@@ -94,7 +94,9 @@ struct ChainCtr {
   uint64_t cmp, vis, scan, wr;
 };
 static_assert(sizeof(ChainCtr) == 32, "ChainCtr is carved from 4 dense slots");
-constexpr uint32_t kSmemReserved = 12;  // dense slots per warp holding ChainCtr + ChainConst
+// dense slots per warp above its S dense positions: ChainCtr (4), ChainConst (8), the
+// snapshot-copy mbarrier and its phase word (2)
+constexpr uint32_t kSmemReserved = 14;
 struct DevSnapStore {
   const mc_snap_node* nodes;
   const uint32_t* pidx;  // parent position within the same snapshot, NIL = root
@@ -741,6 +743,35 @@ __device__ void export_image(Chain& C, char* dst) {
   __syncwarp();
 }
 
+// ---- TMA bulk copy (global -> shared) completing on an mbarrier: the dense list of a
+// chain's snapshot image lands in shared memory without passing through registers ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one lane: arm the barrier with the byte count and start the copy (16 B aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // order earlier generic accesses first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
 #ifndef MC_COPY_UNROLL
 #define MC_COPY_UNROLL 1
 #endif
@@ -772,24 +803,24 @@ __device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S,
   warp_copy16((uint4*)w.rec(), (const uint4*)(src + 64), 2 * (n + 1));
   warp_copy16((uint4*)w.ids(), (const uint4*)(src + img_off_ids(n)), (uint32_t)(img_al16(4ull * (n + 1)) / 16));
   warp_copy16((uint4*)w.eff64(), (const uint4*)(src + img_off_eff(n)), (n + 2) / 2);
-  {
-    const uint32_t m = n + 1;  // slots 0..n
-    const uint32_t ns = min(m, S);
-    const DenseRec* dn = (const DenseRec*)(src + img_off_dense(n));
-    for (uint32_t b = 0; b < m; b += 32 * kCopyU) {  // SMEM part and global tail
-      DenseRec v[kCopyU];
-#pragma unroll
-      for (int q = 0; q < kCopyU; q++) {
-        const uint32_t i = b + 32 * q + lane;
-        if (i < m) v[q] = dn[i];
-      }
-#pragma unroll
-      for (int q = 0; q < kCopyU; q++) {
-        const uint32_t i = b + 32 * q + lane;
-        if (i < m) *(i < ns ? sd + i : w.tail() + i) = v[q];
-      }
+  // dense list: the shared-memory part [0, ns) by one bulk copy on the TMA engine (its
+  // 16-byte multiple; an odd last entry by lane 0) while the warp copies the rest; the
+  // copy completes on the warp's mbarrier (at sd + S + 12, its phase word beside it)
+  const uint32_t m = n + 1, ns = min(m, S);  // slots 0..n
+  const DenseRec* dn = (const DenseRec*)(src + img_off_dense(n));
+  const uint32_t nb = (ns * 8u) & ~15u;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sd + S + 12);
+  uint32_t* phase = reinterpret_cast<uint32_t*>(sd + S + 13);
+  uint32_t ph = 0;
+  if (lane == 0) {
+    ph = *phase;
+    if (nb) {
+      bulk_g2s(sd, dn, nb, bar);
+      *phase = ph ^ 1u;
     }
+    if (nb / 8 < ns) sd[ns - 1] = dn[ns - 1];
   }
+  for (uint32_t i = ns + lane; i < m; i += 32) w.tail()[i] = dn[i];
   {
     const uint32_t* tpos = (const uint32_t*)(src + img_off_tpos(n));
     const HEnt* tent = (const HEnt*)(src + img_off_tent(n));
@@ -811,6 +842,8 @@ __device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S,
       }
     }
   }
+  ph = __shfl_sync(FULL, ph, 0);
+  if (nb) mbar_wait(bar, ph);
 }
 
 // A chain's initial state from a snapshot image (replaces load_snapshot on the replay
@@ -1383,25 +1416,36 @@ __device__ __forceinline__ uint32_t path_at(const Chain& C, uint32_t my_path, ui
 // first token (loaded during request r-1); this request loads request r+1's header
 // at its start, its first token after the walk, and prefetches the child-index line
 // of its root lookup into L2 -- three dependent round trips off the critical path.
+struct ReqHdr {
+  uint32_t off, lin, lout;
+};
 struct Prefetched {
-  mc_request q;
+  ReqHdr q;
   uint32_t tk0;
 };
+__device__ __forceinline__ ReqHdr load_req(const KParams& P, uint32_t r) {
+  const mc_request m = P.req[r - 1];
+  ReqHdr h;
+  h.off = (uint32_t)m.tok_off;
+  h.lin = m.input_len;
+  h.lout = m.output_len;
+  return h;
+}
 __device__ __forceinline__ Prefetched fetch_request(const KParams& P, uint32_t r) {
   Prefetched f;
-  f.q = P.req[r - 1];
-  f.tk0 = __ldg(P.tok + f.q.tok_off);
+  f.q = load_req(P, r);
+  f.tk0 = __ldg(P.tok + f.q.off);
   return f;
 }
 
 __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const Prefetched cur, Prefetched& nxt,
                                   bool has_next, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
-  const mc_request q = cur.q;
-  const uint64_t off = q.tok_off;
-  const uint32_t L_in = q.input_len;
-  const uint32_t n = q.input_len + q.output_len;
-  if (has_next) nxt.q = P.req[r];  // request r+1
+  const ReqHdr q = cur.q;
+  const uint32_t off = q.off;
+  const uint32_t L_in = q.lin;
+  const uint32_t n = q.lin + q.lout;
+  if (has_next) nxt.q = load_req(P, r + 1);  // request r+1
 
   PHASE_T0();
   // Step 1: walk = lookup + speculative insertion bookkeeping.
@@ -1449,7 +1493,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
   CTR_ADD(C, cmp, min(m + 1, n));
   CTR_ADD(C, vis, npath + 1);
   if (has_next) {
-    nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
+    nxt.tk0 = __ldg(P.tok + nxt.q.off);
     if (lane == 0) {
       const HEnt* line = C.w.tab() + hslot(0, nxt.tk0, C.hmask);
       asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
@@ -1814,13 +1858,13 @@ __device__ void evict_lru_blocks(Chain& C, const KParams& P, uint32_t r, uint32_
 __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, const Prefetched cur,
                                        Prefetched& nxt, bool has_next, mc_evict_rec* log, uint32_t* log_n) {
   const uint32_t lane = lane_id();
-  const mc_request q = cur.q;
-  const uint64_t off = q.tok_off;
-  const uint32_t L_in = q.input_len;
-  const uint32_t n = q.input_len + q.output_len;
+  const ReqHdr q = cur.q;
+  const uint32_t off = q.off;
+  const uint32_t L_in = q.lin;
+  const uint32_t n = q.lin + q.lout;
   const uint32_t x = C.block;
   const uint32_t nb = n / x;  // full blocks; a trailing partial block is not cached (V2)
-  if (has_next) nxt.q = P.req[r];
+  if (has_next) nxt.q = load_req(P, r + 1);
   uint32_t* __restrict__ path = C.w.path();
 
   // Step 1: walk block by block (V1).  Block hashes are computed 32 at a time, one
@@ -1849,7 +1893,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   __syncwarp();
   CTR_ADD(C, cmp, (uint64_t)mb * x);
   CTR_ADD(C, vis, mb + 1);
-  if (has_next) nxt.tk0 = __ldg(P.tok + nxt.q.tok_off);
+  if (has_next) nxt.tk0 = __ldg(P.tok + nxt.q.off);
 
   // Step 2: hit = the deepest matched block end <= L_in (V4).
   const uint32_t reuse = min(mb, L_in / x) * x;
