@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target wall time of the oracle sample")
+    p.add_argument("--no-traffic", action="store_true",
+                   help="skip the ncu DRAM-bytes probe of one replay launch (roofline.traffic)")
+    p.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)  # internal: the probe's child
     p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                    help="weak: N independent problems at N GPUs (default); strong: ONE problem's chain list "
                         "LPT-sharded over the N ranks (SURVEY.md d.4; the primary mode for config 5)")
@@ -163,6 +166,16 @@ def algorithmic_bytes(ctr: np.ndarray, n_req_replayed: int) -> int:
 # ----------------------------------------------------------------------------
 # CPU oracle arms (the only places bench.py executes oracle/)
 # ----------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(w, target_s: float, cores: int):
     """A bounded sample of the same workload for the oracle: the first k segments x all
     (variant, α) chains, k sized so the sample takes about target_s seconds on `cores`
@@ -175,6 +188,7 @@ def oracle_sample(w, target_s: float, cores: int):
     t0 = time.perf_counter()
     O.run_chains(tr, [v0], [(0, w.alphas[-1], W + 1, W, 1)], snaps, n_threads=1) if len(snaps) > 1 else None
     per_req = max((time.perf_counter() - t0) / W, 1e-6)
+    oracle_sample.single_thread_rate = 1.0 / per_req
     nchain_per_seg = len(w.alphas) * len(w.variants)
     k = int(max(1, min(len(w.segments()), target_s * cores / (per_req * W * nchain_per_seg))))
     segs = w.segments()[:k]
@@ -201,7 +215,8 @@ def cpu_baseline(w, target_s):
     cores = os.cpu_count() or 1
     snaps, chains, k = oracle_sample(w, target_s, cores)
     n, dt = run_oracle(w, snaps, chains, cores)
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "single_thread_rate": getattr(oracle_sample, "single_thread_rate", None),
             "sample": f"first {k} of {len(w.segments())} segments x {len(w.variants)} variant(s) x "
                       f"{len(w.alphas)} alphas = {len(chains)} chains, "
                       f"{n} request-replays in {dt:.2f} s (snapshots from the oracle's own live pass, untimed)"}
@@ -225,7 +240,8 @@ def reference_arm(args, w, config):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64",
             "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                             "single_thread_rate": getattr(oracle_sample, "single_thread_rate", None),
                              "sample": f"{len(chains)} chains of the first {k} segments per step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -301,7 +317,7 @@ def main():
     t_setup = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream()
     streams = [torch.cuda.Stream() for _ in gs] if len(gs) > 1 else [stream]
-    outs = [g.ctx.alloc_outputs(len(w.alphas), counters=True) for g in gs]
+    outs = [g.ctx.alloc_outputs(len(w.alphas), counters=True, chain_cycles=True) for g in gs]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     my_reqs = sum(int(sum(g.segs[c % len(g.segs)][1] for c in g.chains)) for g in gs)
     all_reqs = sum(sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants) for g in gs)
@@ -326,6 +342,11 @@ def main():
         tot = gather_hit_sums(hs, world)                        # one all-gather over NCCL
         return [g.select(o, gathered=tot[k]) for k, (g, o) in enumerate(zip(gs, outs))]
 
+    if args.traffic_probe:  # child of traffic_probe(): one warm launch, then the launch ncu measures
+        for _ in range(2):
+            launch()
+            torch.cuda.synchronize()
+        return
     for _ in range(args.warmup):
         launch()
         select()
@@ -372,16 +393,19 @@ def main():
     kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1000.0
     peak, peak_kind = peaks()
     achieved = alg_bytes / kern_avg_s / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "replay_traffic.json")
-    if os.path.exists(tp):
-        try:
-            for tj in json.load(open(tp)):  # one entry per (config, n_gpus, policy) capture
-                if (tj.get("config") == args.config and tj.get("n_gpus", 1) == world
-                        and tj.get("policy", "marconi") == args.policy):
-                    traffic = tj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    # d.3 split of the algorithmic bytes and per-request facts of the latency-bound kernel
+    csum = sum(o["counters"].cpu().numpy()[g.chains.astype(np.int64)].astype(np.int64).sum(0)
+               for g, o in zip(gs, outs))
+    split = {"compare_8c": int(W_CMP * csum[0]), "visit_16v": int(W_VIS * csum[1]),
+             "scan_13N": int(W_SCAN * csum[2]), "write_32w": int(W_WR * csum[3]), "outputs_16": int(W_OUT * my_reqs)}
+    cyc = np.concatenate([o["cycles"].cpu().numpy()[g.chains.astype(np.int64)].astype(np.float64) * 1024 /
+                          np.array([g.segs[c % len(g.segs)][1] for c in g.chains], np.float64)
+                          for g, o in zip(gs, outs)])
+    per_request = {"cycles_median": float(np.median(cyc)), "compared_positions": float(csum[0] / my_reqs),
+                   "levels_visited": float(csum[1] / my_reqs), "nodes_scanned": float(csum[2] / my_reqs),
+                   "records_written": float(csum[3] / my_reqs)}
+    traffic, probe = (None, "skipped (--no-traffic)") if args.no_traffic else \
+        ((None, "not run at N > 1 (ncu wraps one process)") if world > 1 else traffic_probe(args))
 
     # e2e through the public API with host buffers (this rank's shards of every problem)
     e2e = None
@@ -395,7 +419,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": T_ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": T_ms / args.steps,
+            "ms_per_step_median": float(np.median(step_ms)), "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
             "config": dict(config, parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one "
                                                  f"{'gloo' if shared else 'NCCL'} all-gather of per-(problem, alpha) "
@@ -405,7 +430,16 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "replay_kernel<%d>" % (args.policy == "vllm"), "alg_bytes_per_launch": alg_bytes,
-                         "launch_ms": kern_avg_s * 1000.0},
+                         "launch_ms": kern_avg_s * 1000.0, "d3_split": split,
+                         "dram_gbs": (traffic / kern_avg_s / 1e9) if traffic else None,
+                         "dram_frac": (traffic / kern_avg_s / 1e9 / peak) if traffic else None,
+                         "traffic_probe": probe, "per_request": per_request,
+                         "note": ("latency-bound: achieved/frac count SURVEY d.3 algorithmic bytes, whose "
+                                  f"{split['scan_13N'] / max(1, alg_bytes):.0%} scan term (13 B per live node per "
+                                  "eviction) is served from shared memory; dram_frac is the measured DRAM "
+                                  "traffic of the same launch" +
+                                  ("; frac > 1.2 means the SMEM-served scan bytes alone exceed the HBM peak, "
+                                   "not that HBM is saturated" if achieved / peak > 1.2 else ""))},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * len(gs),  # one replay_kernel launch per problem per step
@@ -416,63 +450,94 @@ def main():
         dist.destroy_process_group()
 
 
+def traffic_probe(args):
+    """DRAM bytes of one replay launch of this workload, measured by ncu in a child process
+    (`bench.py --traffic-probe`: setup, one warm launch, the measured launch).  Only the
+    byte counters are taken from the profiled run, never a time.  Returns (bytes, how)."""
+    metrics = "dram__bytes_read.sum,dram__bytes_write.sum"
+    cmd = ["ncu", "--metrics", metrics, "--clock-control", "none", "-k", "regex:replay_kernel", "-s", "1", "-c", "1",
+           "--csv", sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", str(args.config),
+           "--policy", args.policy, "--blocks", args.blocks, "--caps-gb", args.caps_gb]
+    if args.requests:
+        cmd += ["--requests", str(args.requests)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except (OSError, subprocess.TimeoutExpired) as e:
+        return None, f"ncu probe failed: {type(e).__name__}"
+    import csv
+    import io
+    tot, seen = 0.0, set()
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    for row in csv.reader(io.StringIO(r.stdout)):
+        if len(row) > 3 and row[-3] in metrics.split(","):
+            try:
+                tot += float(row[-1].replace(",", "")) * scale.get(row[-2], 1)
+                seen.add(row[-3])
+            except ValueError:
+                pass
+    if len(seen) != 2:
+        return None, "ncu probe gave no DRAM counters (rc %d)" % r.returncode
+    return tot, "ncu dram__bytes_read.sum + dram__bytes_write.sum of one replay_kernel launch (child process)"
+
+
 def e2e_measure(gs, ws, args, outs, shared=False):
-    """Same metric end to end through the C ABI from host buffers: per step, for every
-    problem, H2D of the trace (tokens + requests, pinned) and of the segment snapshots,
-    the replay of this rank's chains, D2H of the per-request hits and the hit sums."""
+    """Same metric end to end through the public API from host buffers (grid.HostPipeline):
+    per step and problem, H2D of the trace (tokens + requests, pinned) and of the packed
+    segment snapshots, the device-side trace check, the snapshot images, the replay of this
+    rank's chains, D2H of the per-request hits and the hit sums, α* on the host.  Two
+    slots alternate, so step k+1's transfers run under step k's replay (wall clock over
+    the steady state, the pipeline drained at the end)."""
     import torch
     from paper_2411_19379_b200 import marconi as M
-    st = []
-    for g, wk, o in zip(gs, ws, outs):
+    from paper_2411_19379_b200.grid import HostPipeline
+    jobs = []
+    for g, wk in zip(gs, ws):
         tr = wk.trace
-        ctx = g.ctx
         h_tok = torch.from_numpy(np.ascontiguousarray(tr.tokens, np.uint32).view(np.int32)).pin_memory()
         h_req = torch.from_numpy(M.requests_array(tr.off, tr.lin, tr.lout).view(np.int64)).pin_memory()
-        # host input buffers: the segment snapshots packed once into pinned memory
         snaps = []
         for v in range(len(wk.variants)):
-            nodes, off, nid = ctx.pack_snapshots([ctx.get_snapshot(v, k) for k in range(ctx.snapshot_count(v))])
+            nodes, off, nid = g.ctx.pack_snapshots([g.ctx.get_snapshot(v, k) for k in range(g.ctx.snapshot_count(v))])
             pin = torch.empty(nodes.nbytes, dtype=torch.uint8).pin_memory()
             pnodes = pin.numpy().view(M.SNAP_DTYPE)
             pnodes[:] = nodes
-            snaps.append((pin, pnodes, off, nid))
-        d_tok = torch.empty_like(h_tok, device="cuda")
-        d_req = torch.empty_like(h_req, device="cuda")
-        h_hit = torch.empty(o["hit"].shape, dtype=torch.int32).pin_memory()
-        st.append((g, tr, ctx, o, h_tok, h_req, snaps, d_tok, d_req, h_hit))
-    h2d = sum(x[4].numel() * 4 + x[5].numel() * 8 + sum(sv[1].nbytes + sv[2].nbytes + sv[3].nbytes for sv in x[6])
-              for x in st)
-    d2h = sum(x[9].numel() * 4 + x[3]["hit_sum"].numel() * 8 for x in st)
+            snaps.append((pnodes, off, nid, pin))
+        jobs.append((HostPipeline(g), h_tok, h_req, [(a, b, c) for a, b, c, _ in snaps], snaps))
+    h2d = sum(j[1].numel() * 4 + j[2].numel() * 8 + sum(a.nbytes + b.nbytes + c.nbytes for a, b, c in j[3])
+              for j in jobs)
+    d2h = sum(int(np.prod(o["hit"].shape)) * 4 + o["hit_sum"].numel() * 8 for o in outs)
     n_units = sum(sum(n for _, n, _ in g.segs) * len(wk.alphas) * len(wk.variants) for g, wk in zip(gs, ws))
+    ref = [o["hit_sum"].cpu().numpy() for o in outs]
 
-    def one():
-        for g, tr, ctx, o, h_tok, h_req, snaps, d_tok, d_req, h_hit in st:
-            d_tok.copy_(h_tok, non_blocking=True)
-            d_req.copy_(h_req, non_blocking=True)
-            ctx.set_trace_device(d_tok, d_req, tr.n_requests)
-            for v, (_, pnodes, off, nid) in enumerate(snaps):
-                ctx.set_snapshots_packed(v, pnodes, off, nid)
-            o["hit_sum"].zero_()
-            g.run(out=o)
-            h_hit.copy_(o["hit"], non_blocking=True)
-            g.select(o)
-        torch.cuda.synchronize()
+    def run(steps):
+        pending = []
+        for _ in range(steps):
+            pending.append([p.submit(ht, hr, sn) for p, ht, hr, sn, _ in jobs])
+            if len(pending) > 1:
+                for (p, *_), t in zip(jobs, pending.pop(0)):
+                    p.result(t)
+        res = None
+        for tick in pending:
+            res = [p.result(t) for (p, *_), t in zip(jobs, tick)]
+        return res
 
-    for _ in range(2):
-        one()
+    run(2)
     steps = max(3, args.steps // 2)
     t0 = time.perf_counter()
-    for _ in range(steps):
-        one()
+    res = run(steps)
     dt = time.perf_counter() - t0
+    # the pipelined result equals the kernel-only run's (same chains, same inputs)
+    same = all(np.array_equal(r[1], h) for r, h in zip(res, ref))
     import torch.distributed as dist
     if dist.is_initialized():
         t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t[0])
     return {"value": n_units * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "note": "wall clock incl. H2D of trace+requests and of the packed segment snapshots (pinned host buffers), snapshot image build, replay, D2H of per-request hits"}
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "hit_sums_match_kernel_run": bool(same),
+            "note": "wall clock over pipelined steps (2 slots: step k+1's H2D of trace+requests+packed segment "
+                    "snapshots, device trace check and snapshot images run under step k's replay), incl. D2H of "
+                    "per-request hits and hit sums and alpha* on the host"}
 
 
 if __name__ == "__main__":

@@ -136,10 +136,23 @@ void mc_destroy(mc_ctx* ctx);
 mc_status mc_set_trace(mc_ctx* ctx, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
                        uint32_t n_reqs);
 
+/* The same, validated on the device instead (no request table travels back to the
+ * host): a check kernel on `stream` applies the rules above plus the longest
+ * admissible request (2^20 tokens and F(L) < 2^53, Appendix A); a violation makes
+ * the replay and live kernels on that stream read nothing and the next mc_check
+ * return MC_EINVAL naming the first bad request.  Scalar arguments are validated
+ * synchronously.  The end-to-end path of bench.py uses it. */
+mc_status mc_set_trace_async(mc_ctx* ctx, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
+                             uint32_t n_reqs, void* stream);
+
 /* Upload n_snapshots canonical snapshots for `variant` from host memory:
  * snapshot k is h_nodes[h_offsets[k] .. h_offsets[k+1]) with next node id
  * h_next_id[k].  Records may be in any order; parent links are resolved on the
- * device.  Replaces the variant's snapshot store.  Synchronous on `stream`. */
+ * device.  Replaces the variant's snapshot store.  Asynchronous on `stream`:
+ * records are validated on the host before return, parent links on the device
+ * (mc_check reports a broken link); pageable host arrays may be reused on return,
+ * page-locked h_nodes must stay unchanged until the stream has passed the call.
+ * Work on other streams must not replay this context while the upload runs. */
 mc_status mc_set_snapshots(mc_ctx* ctx, uint32_t variant, const mc_snap_node* h_nodes, const uint64_t* h_offsets,
                            const uint32_t* h_next_id, uint32_t n_snapshots, void* stream);
 

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     if (lane == 0) qi = atomicAdd(P.queue, 1u);
     qi = __shfl_sync(FULL, qi, 0);
     if (qi >= P.n_chains) return;
+    if (*(volatile uint32_t*)P.status & ST_BADTRACE) return;  // rejected trace: read nothing
     const long long t0 = clock64();
     const uint32_t c = P.chains[qi];
     const uint32_t s = c % P.n_segs;
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   const uint32_t lane = lane_id();
   const uint32_t v = blockIdx.x;
   if (v >= P.n_var) return;
+  if (*(volatile uint32_t*)P.status & ST_BADTRACE) return;  // rejected trace: read nothing
   Chain C;
   const uint32_t S = P.smem_nodes - kSmemReserved;
   chain_init(C, P, v, P.var[v], 0.0, smem, S, reinterpret_cast<ChainConst*>(smem + 8ull * (S + 4)),
@@ -196,6 +198,21 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
     }
   }
   if (lane == 0 && P.first_evict) P.first_evict[v] = first;
+}
+
+// Device-side trace check (mc_set_trace_async): the same rules as mc_set_trace's host
+// pass; a violation sets ST_BADTRACE and records the first bad request (1-based) in
+// status[1], so no request table ever travels back to the host.
+__global__ void trace_check_kernel(const mc_request* req, uint32_t n_reqs, uint64_t n_tok, uint32_t lmax,
+                                   uint32_t* status) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_reqs; i += gridDim.x * blockDim.x) {
+    const mc_request q = req[i];
+    const uint64_t n = (uint64_t)q.input_len + q.output_len;
+    if (q.input_len == 0 || n > lmax || q.tok_off + n > n_tok) {
+      atomicOr(status, ST_BADTRACE);
+      atomicMin(status + 1, i + 1);
+    }
+  }
 }
 
 // parent_idx of uploaded canonical records (sorted by id within each snapshot).
@@ -335,7 +352,8 @@ DevModel make_model(const mc_model& m) {
   return d;
 }
 
-mc_status upload_stores(mc_ctx* c) {
+// (asynchronous on st: the staging of the pageable host array completes before return)
+mc_status upload_stores(mc_ctx* c, cudaStream_t st = nullptr) {
   std::vector<DevSnapStore> h(c->snaps.size());
   for (size_t v = 0; v < c->snaps.size(); v++) {
     h[v].nodes = c->snaps[v].nodes;
@@ -348,7 +366,7 @@ mc_status upload_stores(mc_ctx* c) {
     h[v].count = c->snaps[v].count;
     h[v].pad = 0;
   }
-  CU(cudaMemcpy(c->d_stores, h.data(), sizeof(DevSnapStore) * h.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpyAsync(c->d_stores, h.data(), sizeof(DevSnapStore) * h.size(), cudaMemcpyHostToDevice, st));
   return MC_OK;
 }
 
@@ -367,7 +385,7 @@ mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st, const uint32_t* h
     s.img_off = nullptr;
     s.img_cap = 0;
     s.img_off_cap = 0;
-    return upload_stores(c);
+    return upload_stores(c, st);
   }
   std::vector<uint32_t> n(s.count);
   if (host_n) {
@@ -396,7 +414,7 @@ mc_status build_images(mc_ctx* c, uint32_t v, cudaStream_t st, const uint32_t* h
     s.img_off_cap = s.count + 1;
   }
   CU(cudaMemcpyAsync(s.img_off, off.data(), sizeof(uint64_t) * (s.count + 1), cudaMemcpyHostToDevice, st));
-  mc_status rc = upload_stores(c);
+  mc_status rc = upload_stores(c, st);
   if (rc != MC_OK) return rc;
   const uint32_t nb = std::min<uint32_t>(s.count, 4u * (uint32_t)c->n_sm);
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
@@ -502,12 +520,13 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
   c->alpha_cap = (uint32_t)((kCtrl - kAlphaOff) / sizeof(double));  // 256
   if (cudaMalloc(&c->d_var, sizeof(DevVariant) * n_var) != cudaSuccess ||
       cudaMalloc(&c->d_stores, sizeof(DevSnapStore) * n_var) != cudaSuccess ||
-      cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess) {
+      cudaMalloc(&c->d_status, 2 * sizeof(uint32_t)) != cudaSuccess) {
     mc_destroy(c);
     return fail(MC_ENOMEM, "mc_create: device allocation failed");
   }
   cudaMemcpy(c->d_var, c->dvh.data(), sizeof(DevVariant) * n_var, cudaMemcpyHostToDevice);
   cudaMemset(c->d_status, 0, sizeof(uint32_t));
+  cudaMemset(c->d_status + 1, 0xFF, sizeof(uint32_t));  // first rejected request: none
   if (upload_stores(c) != MC_OK) {
     mc_destroy(c);
     return MC_ECUDA;
@@ -548,6 +567,33 @@ mc_status mc_set_trace(mc_ctx* c, const uint32_t* d_tokens, uint64_t n_tokens, c
     unsigned __int128 F = (unsigned __int128)d.m.fa * Lmax + (unsigned __int128)d.m.fb * Lmax * Lmax;
     if (F >= ((unsigned __int128)1 << 53)) return fail(MC_EINVAL, "F(L) exceeds 2^53 for the longest request");
   }
+  c->tok = d_tokens;
+  c->n_tok = n_tokens;
+  c->req = d_reqs;
+  c->n_req = n_reqs;
+  return MC_OK;
+}
+
+mc_status mc_set_trace_async(mc_ctx* c, const uint32_t* d_tokens, uint64_t n_tokens, const mc_request* d_reqs,
+                             uint32_t n_reqs, void* stream) {
+  if (!c || !d_tokens || !d_reqs || n_reqs == 0) return fail(MC_EINVAL, "mc_set_trace_async: null/empty argument");
+  if (n_reqs >= (1u << 30)) return fail(MC_EINVAL, "too many requests (timestamps must stay < 2^30)");
+  if (n_tokens > 0xFFFFFFFFull) return fail(MC_EINVAL, "token pool must hold < 2^32 tokens (u32 node offsets)");
+  // longest admissible request: <= 2^20 tokens and F(L) < 2^53 for every variant
+  uint32_t lmax = 1u << 20;
+  for (const auto& d : c->dvh) {
+    const auto F = [&](uint64_t L) { return (unsigned __int128)d.m.fa * L + (unsigned __int128)d.m.fb * L * L; };
+    uint32_t lo = 0, hi = lmax;  // largest L <= lmax with F(L) < 2^53 (F is increasing)
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo + 1) / 2;
+      if (F(mid) < ((unsigned __int128)1 << 53)) lo = mid; else hi = mid - 1;
+    }
+    lmax = lo;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = (int)std::min<uint32_t>((n_reqs + 255) / 256, 148 * 4);
+  trace_check_kernel<<<blocks, 256, 0, st>>>(d_reqs, n_reqs, n_tokens, lmax, c->d_status);
+  CU(cudaGetLastError());
   c->tok = d_tokens;
   c->n_tok = n_tokens;
   c->req = d_reqs;
@@ -611,9 +657,8 @@ mc_status mc_set_snapshots(mc_ctx* c, uint32_t variant, const mc_snap_node* h_no
   dim3 grid(8, n_snap);
   snap_link_kernel<<<grid, 256, 0, st>>>(s.nodes, s.off, n_snap, s.pidx, c->d_status);
   CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(st));
   s.count = n_snap;
-  mc_status rc = upload_stores(c);
+  mc_status rc = upload_stores(c, st);
   if (rc != MC_OK) return rc;
   return build_images(c, variant, st, cnt.data());
 }
@@ -891,10 +936,16 @@ mc_status mc_eviction_log(mc_ctx* c, const mc_replay_args* A, uint32_t v, uint32
 mc_status mc_check(mc_ctx* c, void* stream) {
   if (!c) return fail(MC_EINVAL, "mc_check: null context");
   CU(cudaStreamSynchronize((cudaStream_t)stream));
-  uint32_t st = 0;
-  CU(cudaMemcpy(&st, c->d_status, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  uint32_t sw[2] = {0, 0};
+  CU(cudaMemcpy(sw, c->d_status, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  const uint32_t st = sw[0];
   if (st) {
     cudaMemset(c->d_status, 0, sizeof(uint32_t));
+    cudaMemset(c->d_status + 1, 0xFF, sizeof(uint32_t));
+    if (st & ST_BADTRACE)
+      return fail(MC_EINVAL, "trace rejected by the device check: request " + std::to_string(sw[1]) +
+                                 " has input_len == 0, a range outside the pool, or is too long (2^20 tokens / "
+                                 "F(L) < 2^53)");
     std::string m = "device status:";
     if (st & ST_OVERFLOW) m += " node-table overflow (raise max_nodes);";
     if (st & ST_INVARIANT) m += " invariant violated (capacity / hit <= input / snapshot);";

@@ -63,6 +63,7 @@ enum : uint32_t {
   ST_INVARIANT = 2u,  // capacity exceeded after admission / hit > input / bad snapshot
   ST_NOCAND = 4u,     // eviction needed but no candidate (cannot happen after the precheck)
   ST_SNAPOVF = 8u,    // snapshot store too small
+  ST_BADTRACE = 16u,  // the device-side trace check (mc_set_trace_async) rejected a request
 };
 
 // Cost model constants (Appendix A tab:flops_breakdown PAPER:771-772),

@@ -209,3 +209,88 @@ class LiveTuner:
             hits[b_end:] = out2["hit"].cpu().numpy()[0, ai, b_end:]
             flops[b_end:] = out2["flops"].cpu().numpy()[0, ai, b_end:]
         return hits, flops, info
+
+
+class HostPipeline:
+    """End-to-end α-grid replay from HOST buffers, double-buffered (the path a serving
+    system's tuner takes when each tuning job arrives in host memory).
+
+    Per job: H2D of the trace (tokens + request table) and of the packed segment
+    snapshots, the device-side trace check (mc_set_trace_async), the snapshot images,
+    the replay of `grid`'s chain shard, D2H of the per-request hits and the per-α hit
+    sums, α* on the host.  Two slots (each its own context, device buffers, workspace
+    and outputs) alternate: job k+1's copies and image build run on a copy stream while
+    job k replays on the compute stream, so the transfers hide under the replay.  Every
+    step of the path runs in libmarconi's kernels; this class only sequences streams.
+
+    grid: a set-up AlphaGrid (its segments, chain shard and variants are reused).
+    """
+
+    def __init__(self, grid: "AlphaGrid", n_slots: int = 2):
+        import torch
+        self.torch = torch
+        self.g = grid
+        self.copy_stream = torch.cuda.Stream()
+        self.compute_stream = torch.cuda.Stream()
+        self.slots = []
+        for _ in range(n_slots):
+            ctx = M.Context(grid.variants, max_nodes=grid.ctx.max_nodes, device=grid.ctx.device.index or 0)
+            self.slots.append({"ctx": ctx, "ws": ctx.alloc_workspace(0, len(grid.alphas), len(grid.chains)),
+                               "d_tok": None, "d_req": None, "out": None, "h_hit": None, "h_hs": None,
+                               "done": None})
+        self.k = 0
+
+    def submit(self, h_tok, h_req, snapshots):
+        """Queue one job.  h_tok: pinned int32 tensor of tokens; h_req: pinned int64 tensor
+        holding REQUEST_DTYPE records; snapshots: per variant (nodes SNAP_DTYPE in pinned
+        memory, offsets u64, next ids u32) as from Context.pack_snapshots.  Returns a ticket."""
+        torch = self.torch
+        s = self.slots[self.k % len(self.slots)]
+        ctx = s["ctx"]
+        n_req = h_req.numel() * 8 // M.REQUEST_DTYPE.itemsize
+        if s["d_tok"] is None or s["d_tok"].numel() != h_tok.numel() or s["d_req"].numel() != h_req.numel():
+            s["d_tok"] = torch.empty(h_tok.shape, dtype=h_tok.dtype, device=ctx.device)
+            s["d_req"] = torch.empty(h_req.shape, dtype=h_req.dtype, device=ctx.device)
+        cs, ks = self.copy_stream, self.compute_stream
+        if s["done"] is not None:
+            cs.wait_event(s["done"])  # the slot's previous job has left its buffers
+        with torch.cuda.stream(cs):
+            s["d_tok"].copy_(h_tok, non_blocking=True)
+            s["d_req"].copy_(h_req, non_blocking=True)
+            ctx.set_trace_async(s["d_tok"], s["d_req"], n_req, stream=cs)
+            if ctx.segments is None:
+                ctx.set_segments(self.g.segs)  # (validated against the request count: once, after the trace)
+            for v, (nodes, off, nid) in enumerate(snapshots):
+                ctx.set_snapshots_packed(v, nodes, off, nid, stream=cs)
+            ready = torch.cuda.Event()
+            ready.record(cs)
+        if s["out"] is None or s["out"]["hit"].shape[-1] != n_req:
+            s["out"] = ctx.alloc_outputs(len(self.g.alphas))
+            s["h_hit"] = torch.empty(s["out"]["hit"].shape, dtype=torch.int32).pin_memory()
+            s["h_hs"] = torch.empty(s["out"]["hit_sum"].shape, dtype=torch.int64).pin_memory()
+        ks.wait_event(ready)
+        with torch.cuda.stream(ks):
+            s["out"]["hit_sum"].zero_()
+            ctx.replay(self.g.alphas, chains=self.g.chains, workspace=s["ws"], out=s["out"], stream=ks)
+            s["h_hit"].copy_(s["out"]["hit"], non_blocking=True)
+            s["h_hs"].copy_(s["out"]["hit_sum"], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(ks)
+        s["done"] = done
+        t = self.k
+        self.k += 1
+        return t
+
+    def result(self, ticket):
+        """Wait for job `ticket` (the most recent len(slots) jobs stay retrievable);
+        returns (hits int32[n_var, n_alpha, R] host tensor, hit sums, α* per variant)."""
+        s = self.slots[ticket % len(self.slots)]
+        s["done"].synchronize()
+        s["ctx"].check(stream=self._idle())  # device status of this slot's context
+        hs = s["h_hs"].numpy()
+        return s["h_hit"], hs, select_alpha(self.g.alphas, hs)
+
+    def _idle(self):
+        if not hasattr(self, "_idle_stream"):
+            self._idle_stream = self.torch.cuda.Stream()
+        return self._idle_stream

@@ -25,7 +25,7 @@ EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n
                         ("utility", "<f8")], align=True)
 assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
 
-EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at",
+EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at",
             "mc_snapshot_count",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
             "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log")
@@ -74,6 +74,7 @@ def lib():
         for name, args in {
             "mc_create": [P, U32, U32, I, P],
             "mc_set_trace": [P, P, U64, P, U32],
+            "mc_set_trace_async": [P, P, U64, P, U32, P],
             "mc_set_snapshots": [P, U32, P, P, P, U32, P],
             "mc_live_pass": [P, U32, P, U64, P, P, P, P],
             "mc_live_pass_at": [P, P, U32, P, U64, P, P, P, P, P],
@@ -178,6 +179,13 @@ class Context:
         """d_tokens: int32/uint32 CUDA tensor; d_reqs: CUDA tensor holding REQUEST_DTYPE records."""
         self._keep = [d_tokens, d_reqs]
         check(lib().mc_set_trace(self.h, _tptr(d_tokens), d_tokens.numel(), _tptr(d_reqs), int(n_reqs)))
+        self.n_req = int(n_reqs)
+
+    def set_trace_async(self, d_tokens, d_reqs, n_reqs: int, stream=None):
+        """As set_trace_device, validated by a device kernel on `stream` (errors at check())."""
+        self._keep = [d_tokens, d_reqs]
+        check(lib().mc_set_trace_async(self.h, _tptr(d_tokens), d_tokens.numel(), _tptr(d_reqs), int(n_reqs),
+                                       _stream_ptr(stream)))
         self.n_req = int(n_reqs)
 
     def upload_trace(self, tokens: np.ndarray, off, lin, lout, stream=None):
