@@ -173,6 +173,16 @@ mc_status mc_live_pass_at(mc_ctx* ctx, const uint32_t* h_points, uint32_t n_poin
                           uint64_t workspace_bytes, uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass,
                           uint32_t* h_first_evict, void* stream);
 
+/* The paper's tuning pass in ONE live pass (§4.2 "Managing the balance"):
+ * α = 0 from the empty cache; the first request r_F whose admission evicts is found on
+ * the fly; snapshot 1 = the tree after r_F, snapshot 2 = the tree after
+ * r_F + multiplier * r_F (when that is < n_reqs), snapshot 0 = empty; a snapshot the
+ * pass never reaches stays empty.  h_first_evict receives r_F per variant (0 = no
+ * eviction).  Per-request outputs and workspace as mc_live_pass_at; multiplier >= 1. */
+mc_status mc_live_pass_bootstrap(mc_ctx* ctx, uint32_t multiplier, void* d_workspace, uint64_t workspace_bytes,
+                                 uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict,
+                                 void* stream);
+
 /* Number of snapshots held for a variant and copy one back as canonical
  * records sorted by id (host).  *n_out receives the record count; h_out may be
  * NULL to query it. */

@@ -178,23 +178,33 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   load_snapshot(C, P, nullptr, 0);  // empty tree
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
-  uint32_t next = 1, first = 0;
+  uint32_t next = 1, first = 0, boot_end = 0;
   Prefetched cur = fetch_request(P, 1), nxt = cur;
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
     const uint32_t ev0 = C.n_evict;
     const ReqOut o = C.block ? process_request_vllm(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr)
                              : process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
     cur = nxt;
-    if (first == 0 && C.n_evict != ev0) first = r;  // the paper's "first eviction"
+    if (first == 0 && C.n_evict != ev0) {  // the paper's "first eviction"
+      first = r;
+      if (P.live_mult) {  // bootstrap mode: the tuning snapshot and the end of the bootstrap window
+        dump_snapshot(C, P, out, 1);
+        boot_end = r + P.live_mult * r;
+      }
+    }
     if (lane == 0) {
       const uint64_t k = (uint64_t)v * P.n_req + r - 1;
       if (P.hit) P.hit[k] = o.reuse;
       if (P.flops) P.flops[k] = o.flops;
       if (P.bypass) P.bypass[k] = o.bypass ? 1 : 0;
     }
-    while (next < P.n_points && P.live_points[next] == r) {
-      dump_snapshot(C, P, out, next);
-      next++;
+    if (P.live_mult) {
+      if (r == boot_end && r < P.n_req) dump_snapshot(C, P, out, 2);
+    } else {
+      while (next < P.n_points && P.live_points[next] == r) {
+        dump_snapshot(C, P, out, next);
+        next++;
+      }
     }
   }
   if (lane == 0 && P.first_evict) P.first_evict[v] = first;
@@ -681,15 +691,13 @@ mc_status mc_workspace_workers(const mc_ctx* c, uint64_t bytes, uint32_t n_alpha
   return MC_OK;
 }
 
-mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points, void* d_ws, uint64_t ws_bytes,
-                          uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict,
-                          void* stream) {
-  if (!c || !d_ws || !h_points || n_points == 0) return fail(MC_EINVAL, "mc_live_pass_at: bad argument");
-  if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
-  if (h_points[0] != 0) return fail(MC_EINVAL, "snapshot point 0 must be 0 (the empty tree)");
-  for (uint32_t k = 1; k < n_points; k++)
-    if (h_points[k] <= h_points[k - 1] || h_points[k] > c->n_req)
-      return fail(MC_EINVAL, "snapshot points must be strictly increasing request indices <= n_reqs");
+namespace {
+// The live pass proper: static snapshot points (mult = 0) or the bootstrap points
+// {0, r_F, r_F + mult r_F} found during the pass (n_points = 3; an undumped snapshot
+// stays empty).
+mc_status live_pass_impl(mc_ctx* c, const uint32_t* h_points, uint32_t n_points, uint32_t mult, void* d_ws,
+                         uint64_t ws_bytes, uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass,
+                         uint32_t* h_first_evict, void* stream) {
   const uint32_t nv = (uint32_t)c->hv.size();
   const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
   if (ws_bytes < kCtrl + per * nv) return fail(MC_ENOMEM, "workspace too small for the live pass");
@@ -726,6 +734,16 @@ mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points
   if (sizeof(DevSnapOut) * nv + 256 > kCtrl) return fail(MC_EINVAL, "too many variants for the live pass");
   CU(cudaMemcpyAsync(d_outs, outs.data(), sizeof(DevSnapOut) * nv, cudaMemcpyHostToDevice, st));
   CU(cudaMemcpyAsync(c->d_points, h_points, sizeof(uint32_t) * K, cudaMemcpyHostToDevice, st));
+  {  // every snapshot starts empty (a bootstrap point the pass never reaches stays so)
+    std::vector<uint64_t> off0(K);
+    std::vector<uint32_t> nid0(K, 1);
+    for (uint32_t k = 0; k < K; k++) off0[k] = (uint64_t)k * c->ncap;
+    for (uint32_t v = 0; v < nv; v++) {
+      CU(cudaMemsetAsync(c->snaps[v].n, 0, sizeof(uint32_t) * K, st));
+      CU(cudaMemcpyAsync(c->snaps[v].off, off0.data(), sizeof(uint64_t) * K, cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpyAsync(c->snaps[v].nid, nid0.data(), sizeof(uint32_t) * K, cudaMemcpyHostToDevice, st));
+    }
+  }
   KParams P;
   memset(&P, 0, sizeof(P));
   P.tok = c->tok;
@@ -747,6 +765,7 @@ mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points
   P.live_points = c->d_points;
   P.n_points = K;
   P.first_evict = c->d_points + K;
+  P.live_mult = mult;
   P.smem_nodes = c->smem_nodes_live;
   live_kernel<<<nv, 32, 8ull * c->smem_nodes_live, st>>>(P);
   CU(cudaGetLastError());
@@ -760,6 +779,27 @@ mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points
   mc_status rc = upload_stores(c);
   for (uint32_t v = 0; v < nv && rc == MC_OK; v++) rc = build_images(c, v, st);
   return rc;
+}
+}  // namespace
+
+mc_status mc_live_pass_at(mc_ctx* c, const uint32_t* h_points, uint32_t n_points, void* d_ws, uint64_t ws_bytes,
+                          uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict,
+                          void* stream) {
+  if (!c || !d_ws || !h_points || n_points == 0) return fail(MC_EINVAL, "mc_live_pass_at: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
+  if (h_points[0] != 0) return fail(MC_EINVAL, "snapshot point 0 must be 0 (the empty tree)");
+  for (uint32_t k = 1; k < n_points; k++)
+    if (h_points[k] <= h_points[k - 1] || h_points[k] > c->n_req)
+      return fail(MC_EINVAL, "snapshot points must be strictly increasing request indices <= n_reqs");
+  return live_pass_impl(c, h_points, n_points, 0, d_ws, ws_bytes, d_hit, d_flops, d_bypass, h_first_evict, stream);
+}
+
+mc_status mc_live_pass_bootstrap(mc_ctx* c, uint32_t multiplier, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,
+                                 uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict, void* stream) {
+  if (!c || !d_ws || multiplier == 0) return fail(MC_EINVAL, "mc_live_pass_bootstrap: bad argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_live_pass before mc_set_trace");
+  const uint32_t pts[3] = {0, 0, 0};  // (dynamic: found during the pass)
+  return live_pass_impl(c, pts, 3, multiplier, d_ws, ws_bytes, d_hit, d_flops, d_bypass, h_first_evict, stream);
 }
 
 mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes, uint32_t* d_hit,

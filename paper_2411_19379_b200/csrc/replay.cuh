@@ -181,6 +181,7 @@ struct KParams {
   const uint32_t* live_points;  // snapshot k = tree after request live_points[k] (ascending, [0] = 0)
   uint32_t n_points;
   uint32_t* first_evict;        // [n_var] first request whose admission evicted (0 = none)
+  uint32_t live_mult;           // > 0: bootstrap points instead (snapshot 1 after r_F, 2 after r_F + mult r_F)
   uint32_t smem_nodes;  // dense positions held in shared memory per warp
 };
 

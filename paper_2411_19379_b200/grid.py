@@ -177,17 +177,17 @@ class LiveTuner:
         tr = self.trace
         R = tr.n_requests
         self.ctx.upload_trace(tr.tokens, tr.off, tr.lin, tr.lout)
-        hit0, fl0, by0, fe = self.ctx.live_pass_at([0])
+        # one live pass: α = 0 outputs for every request plus the snapshots after r_F and
+        # after the bootstrap window, taken as the pass reaches them
+        h1, f1, _, fe = self.ctx.live_pass_bootstrap(self.multiplier)
         r_f = fe[0]
-        hits = hit0[0].cpu().numpy().copy()
-        flops = fl0[0].cpu().numpy().copy()
+        hits = h1[0].cpu().numpy().copy()
+        flops = f1[0].cpu().numpy().copy()
         info = {"r_first_evict": r_f, "alpha_star": 0.0, "window": None, "grid_hit_sums": None}
         if r_f == 0 or r_f >= R:
             return hits, flops, info
         b_end = min(r_f + self.multiplier * r_f, R)
         info["window"] = (r_f + 1, b_end)
-        points = [0, r_f] + ([b_end] if b_end < R else [])
-        h1, f1, _, _ = self.ctx.live_pass_at(points)
         segs = [(r_f + 1, b_end - r_f, 1)]
         if b_end < R:
             segs.append((b_end + 1, R - b_end, 2))
@@ -199,9 +199,6 @@ class LiveTuner:
         a_star = select_alpha(self.alphas, sums[None, :])[0]
         info["alpha_star"] = a_star
         info["grid_hit_sums"] = [int(x) for x in sums]
-        live_hits = h1[0].cpu().numpy()
-        hits[:b_end] = live_hits[:b_end]
-        flops[:b_end] = f1[0].cpu().numpy()[:b_end]
         if b_end < R:
             ai = self.alphas.index(a_star)
             out2 = self.ctx.replay(self.alphas, chains=[ai * ns + 1], log_cap=0)

@@ -25,7 +25,7 @@ EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n
                         ("utility", "<f8")], align=True)
 assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
 
-EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at",
+EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at", "mc_live_pass_bootstrap",
             "mc_snapshot_count",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
             "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log")
@@ -78,6 +78,7 @@ def lib():
             "mc_set_snapshots": [P, U32, P, P, P, U32, P],
             "mc_live_pass": [P, U32, P, U64, P, P, P, P],
             "mc_live_pass_at": [P, P, U32, P, U64, P, P, P, P, P],
+            "mc_live_pass_bootstrap": [P, U32, P, U64, P, P, P, P, P],
             "mc_snapshot_count": [P, U32, P],
             "mc_get_snapshot": [P, U32, U32, P, U64, P, P],
             "mc_set_segments": [P, P, U32],
@@ -274,6 +275,22 @@ class Context:
         fe = np.zeros(nv, np.uint32)
         check(lib().mc_live_pass_at(self.h, _np_ptr(pts), len(pts), _tptr(ws), ws.numel(), _tptr(hit), _tptr(fl),
                                     _tptr(by), _np_ptr(fe), _stream_ptr(stream)))
+        self.check(stream)
+        return hit, fl, by, [int(x) for x in fe]
+
+    def live_pass_bootstrap(self, multiplier: int = 10, workspace=None, stream=None):
+        """One α = 0 live pass that also takes the paper's tuning snapshots:
+        snapshot 1 after the first evicting request r_F, 2 after r_F + multiplier*r_F.
+        Returns (hit, flops, bypass device tensors [n_var, R], r_F list per variant)."""
+        torch = self.torch
+        nv = len(self.variants)
+        ws = workspace if workspace is not None else self.alloc_workspace(n_workers=nv)
+        hit = torch.zeros((nv, self.n_req), dtype=torch.int32, device=self.device)
+        fl = torch.zeros((nv, self.n_req), dtype=torch.int64, device=self.device)
+        by = torch.zeros((nv, self.n_req), dtype=torch.uint8, device=self.device)
+        fe = np.zeros(nv, np.uint32)
+        check(lib().mc_live_pass_bootstrap(self.h, int(multiplier), _tptr(ws), ws.numel(), _tptr(hit), _tptr(fl),
+                                           _tptr(by), _np_ptr(fe), _stream_ptr(stream)))
         self.check(stream)
         return hit, fl, by, [int(x) for x in fe]
 
