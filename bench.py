@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--blocks", default="16,32,64,128", help="vLLM+ block sizes (tokens)")
     p.add_argument("--caps-gb", default="30,60,90,120", help="vLLM+ cache sizes (GB)")
     p.add_argument("--requests", type=int, default=0, help="override R (testing only)")
+    p.add_argument("--layout", default="stream", choices=["stream", "copy"],
+                   help="copy: every request holds its own copy of its sequence (no shared session stream, "
+                        "so every walk level compares tokens; SURVEY.md a2)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target wall time of the oracle sample")
@@ -257,7 +260,7 @@ def main():
     rank, world, local = dist_env()
     n_prob = max(1, world) if (args.impl == "b200" and args.scaling == "weak") else 1
     t_gen = time.perf_counter()
-    ws = [tg.workload(args.config, R=args.requests or None, problem=k) for k in range(n_prob)]
+    ws = [tg.workload(args.config, R=args.requests or None, problem=k, layout=args.layout) for k in range(n_prob)]
     if args.policy == "vllm":  # NEXT-2: the vLLM+ baseline on the same traces, block x cache-size sweep
         blocks = [int(b) for b in args.blocks.split(",")]
         caps = [int(float(c) * tg.GB) for c in args.caps_gb.split(",")]
@@ -276,7 +279,7 @@ def main():
                           (f"; x {n_prob} independent problems (one per GPU, weak scaling)" if n_prob > 1 else "") +
                           (f"; one chain list sharded over {world} ranks (strong scaling)"
                            if args.scaling == "strong" and world > 1 else ""),
-              "requests": tr.n_requests, "tokens": tr.n_tokens, "alphas": len(w.alphas),
+              "requests": tr.n_requests, "tokens": tr.n_tokens, "layout": args.layout, "alphas": len(w.alphas),
               "segments": len(w.segments()), "chains": w.n_chains * n_prob, "window": w.window,
               "problems": n_prob, "policy": args.policy,
               "model": "7B hybrid {4 attn, 24 ssm, 28 mlp}, D=4096, N=128, fp16" if args.config in (2, 3, 4)
@@ -457,7 +460,7 @@ def traffic_probe(args):
     metrics = "dram__bytes_read.sum,dram__bytes_write.sum"
     cmd = ["ncu", "--metrics", metrics, "--clock-control", "none", "-k", "regex:replay_kernel", "-s", "1", "-c", "1",
            "--csv", sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", str(args.config),
-           "--policy", args.policy, "--blocks", args.blocks, "--caps-gb", args.caps_gb]
+           "--policy", args.policy, "--blocks", args.blocks, "--caps-gb", args.caps_gb, "--layout", args.layout]
     if args.requests:
         cmd += ["--requests", str(args.requests)]
     try:

@@ -934,15 +934,31 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
   __syncwarp();
 }
 
-// Warp-cooperative first mismatch of tok[a..a+cmp) vs tok[b..b+cmp).
+// Long compares (up to 32k-token contexts): beyond the
+// first round trip's 32 * kB tokens, lane 0 asks the TMA engine to prefetch the rest of
+// both ranges into L2 (cp.async.bulk.prefetch.L2: one instruction per range, any size),
+// so the following round trips hit L2 instead of DRAM.
+__device__ __forceinline__ void bulk_prefetch_l2(const uint32_t* tok, uint64_t t0, uint64_t t1, uint64_t n_tok) {
+  t0 &= ~3ull;                                   // 16-byte aligned start
+  t1 = min((t1 + 3) & ~3ull, n_tok & ~3ull);     // 16-byte multiple, inside the pool
+  if (t1 > t0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tok + t0), "r"((uint32_t)(4 * (t1 - t0)))
+                 : "memory");
+}
+
+// Warp-cooperative first mismatch of tok[a..a+cmp) vs tok[b..b+cmp) (n_tok: pool size).
 __device__ __forceinline__ uint32_t match_len(const uint32_t* __restrict__ tok, uint64_t a, uint64_t b,
-                                              uint32_t cmp) {
+                                              uint32_t cmp, uint64_t n_tok) {
   if (a == b) return cmp;  // same pool range: identical tokens
   const uint32_t lane = lane_id();
 #ifndef MC_MATCH_BLOCKS
 #define MC_MATCH_BLOCKS 8
 #endif
   constexpr int kB = MC_MATCH_BLOCKS;  // 32-token blocks compared per round trip
+  if (cmp > 32 * kB && lane == 0) {
+    bulk_prefetch_l2(tok, a + 32 * kB, a + cmp, n_tok);
+    bulk_prefetch_l2(tok, b + 32 * kB, b + cmp, n_tok);
+  }
   for (uint32_t base = 0; base < cmp; base += 32 * kB) {
     unsigned mis[kB];
 #pragma unroll
@@ -1469,7 +1485,7 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
     // prefetch the query token the next level will look up
     const uint32_t nt = (de < n) ? __ldg(P.tok + off + de) : 0u;
     const uint32_t cmp = min(len, n - pos);
-    const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, off + pos, cmp);
+    const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, off + pos, cmp, P.n_tok);
     if (lane == 0 && npath >= 32) C.w.path()[npath] = c;
     if (lane == npath) {
       my_path = c; my_ds = pos; my_de = de; my_fl = fl;
@@ -1718,7 +1734,7 @@ __device__ __forceinline__ uint32_t child_block(const Chain& C, const KParams& P
       mm &= mm - 1;
       const uint32_t roff = __shfl_sync(FULL, e.roff, fm);
       const uint32_t key = __shfl_sync(FULL, e.key, fm);
-      if (match_len(P.tok, (uint64_t)roff + kx, b0, x) == x) return key & SLOT14;
+      if (match_len(P.tok, (uint64_t)roff + kx, b0, x, P.n_tok) == x) return key & SLOT14;
     }
     if (me) return NIL;
     seen += lim;

@@ -284,14 +284,14 @@ def test_chain_subsets_and_order_do_not_matter():
         assert torch.equal(out[key], o2[key]), key
 
 
-def _full_grid_parity(cfg, log_chains=()):
+def _full_grid_parity(cfg, log_chains=(), layout="stream"):
     """All chains of BASELINE config `cfg` at full size, in the bench launch configuration
     (eviction logs OFF: the branch bench.py times), against the oracle (live-pass snapshots,
     every request of every chain, d.3 counters, hit sums, α*).  Then a second replay call
     with eviction logs on the `log_chains` subset: logs equal the oracle's bitwise and
     turning logs on changes no output."""
     import os
-    w = tg.workload(cfg)
+    w = tg.workload(cfg, layout=layout)
     tr = w.trace
     g = AlphaGrid(tr, w.variants, w.alphas, w.n_segments).setup()
     out = g.run(counters=True)
@@ -351,6 +351,56 @@ def test_full_config3_sharegpt():
 def test_full_config4_swebench():
     """configs[3]: SWEBench-shaped, contexts up to 32,768 tokens, 2,048 chains."""
     _full_grid_parity(4, log_chains=(5, 9 * 128 + 77))
+
+
+def test_full_config4_copy_layout():
+    """configs[3] with every request holding its own copy of its sequence (no shared session
+    stream, so no compare is skipped): the long-compare path (16-byte loads, funnel-shifted
+    edge side) at full size, 2,048 chains, vs the oracle."""
+    _full_grid_parity(4, log_chains=(5, 9 * 128 + 77), layout="copy")
+
+
+def test_full_config3_copy_layout():
+    """configs[2] in the copy layout: every walk level compares tokens."""
+    _full_grid_parity(3, log_chains=(0, 8 * 128 + 64), layout="copy")
+
+
+def test_long_compare_alignments():
+    """Long shared prefixes (600-3,000 tokens) whose first mismatch falls at every offset
+    class around the vector path's 16-byte quads (head, body, last partial quad, exactly at
+    the end), with request offsets in all four alignments: hits, snapshots and eviction
+    logs equal the oracle's."""
+    rng = np.random.default_rng(77)
+    for seed in range(24):
+        L = int(rng.integers(600, 3000))
+        base = (rng.integers(1, 1 << 30, L)).astype(np.uint32)
+        reqs = []
+        for i in range(14):
+            k = int(rng.choice([0, 1, 2, 3, 4, 5, 127, 128, 129, 511, 512, 513, L - 5, L - 1, L,
+                                int(rng.integers(0, L))]))
+            k = max(0, min(k, L))
+            pad = int(rng.integers(0, 4))  # shifts the request's pool offset modulo 4
+            seq = base[:k].tolist() + [int(x) for x in rng.integers(1 << 30, (1 << 31) - 1, 3 + pad)]
+            cut = int(rng.integers(1, len(seq)))
+            reqs.append((seq[:cut], seq[cut:]))
+        tr = tg.from_sequences(reqs)
+        v = tg.Variant(tg.MODEL_7B, int(rng.choice([2, 4, 8])) * 27_000_000 + 1_000_000_000, 0)
+        alphas = [0.0, 1.0]
+        g, out = GU.gpu_grid(tr, [v], alphas, 2, max_nodes=256, log_cap=128)
+        snaps, live, res, segs = GU.oracle_grid(tr, [v], alphas, 2, threads=1)
+        assert np.array_equal(g.live[0].cpu().numpy()[0], live[0][0]), seed
+        for k in range(len(snaps[0])):
+            gs, gn = g.ctx.get_snapshot(0, k)
+            on, onid = snaps[0][k]
+            assert gn == onid and np.array_equal(GU.canon(gs), GU.canon(on)), (seed, k)
+        hit = out["hit"].cpu().numpy()
+        for cid, (h, f, b, ctr) in res.items():
+            ai, si = cid // len(segs), cid % len(segs)
+            first, n, k = segs[si]
+            assert np.array_equal(hit[0, ai, first - 1:first - 1 + n], h), (seed, cid)
+            _, _, _, lg = GU.oracle_chain_log(tr, v, alphas[ai], first, n, snaps[0][k])
+            glog, gn = g.ctx.read_log(out, cid)
+            _assert_logs_equal(glog, gn, lg, f"long-compare seed {seed} chain {cid}")
 
 
 def test_full_config5_sampled():

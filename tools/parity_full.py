@@ -47,6 +47,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--requests", type=int, default=0)
+    ap.add_argument("--layout", default="stream", choices=["stream", "copy"])
     ap.add_argument("--log-chains", type=int, default=24, help="chains replayed a second time with eviction logs")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
@@ -57,7 +58,7 @@ def main():
     import gpu_util as GU
     from paper_2411_19379_b200 import AlphaGrid
 
-    w = tg.workload(a.config, R=a.requests or None)
+    w = tg.workload(a.config, R=a.requests or None, layout=a.layout)
     tr = w.trace
     nv, na = len(w.variants), len(w.alphas)
     res = {"config": a.config, "workload": w.name, "requests": tr.n_requests, "variants": nv, "alphas": na,

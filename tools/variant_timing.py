@@ -11,7 +11,7 @@ import tracegen as tg
 from paper_2411_19379_b200 import AlphaGrid
 
 cfg = int(os.environ.get("CFG", "3"))
-w = tg.workload(cfg)
+w = tg.workload(cfg, layout=os.environ.get("LAYOUT", "stream"))
 g = AlphaGrid(w.trace, w.variants, w.alphas, w.n_segments, max_nodes=int(os.environ.get('MAXN', '8192'))).setup()
 out = g.ctx.alloc_outputs(len(w.alphas), counters=True, chain_cycles=True)
 ts = []
@@ -29,7 +29,7 @@ for it in range(6):
 g.ctx.check()
 cyc = out["cycles"].cpu().numpy().astype(np.float64) * 1024
 ctr = out["counters"].cpu().numpy()
-print(f"{os.path.basename(os.environ.get('MARCONI_LIB', 'default'))} NW={os.environ.get('NW', '-')} cfg{cfg}: replay ms {np.median(ts[1:]):.2f} "
+print(f"{os.path.basename(os.environ.get('MARCONI_LIB', 'default'))} NW={os.environ.get('NW', '-')} cfg{cfg} {os.environ.get('LAYOUT', 'stream')}: replay ms {np.median(ts[1:]):.2f} "
       f"(min {min(ts[1:]):.2f}) chains {len(g.chains)} chain-cycles median {np.median(cyc)/1e6:.2f}M max {cyc.max()/1e6:.2f}M "
       f"hitsum {int(out['hit_sum'].sum())}", flush=True)
 if os.environ.get("PHASES"):

@@ -153,6 +153,19 @@ class Trace:
         o = int(self.off[i])
         return self.tokens[o:o + int(self.lin[i]) + int(self.lout[i])]
 
+    def copy_layout(self) -> "Trace":
+        """The same requests with every full sequence copied into its own pool range (as
+        an engine that stores each request's tokens separately would hold them): no two
+        requests share pool offsets, so every lookup compares tokens (SURVEY.md §8(a) a2;
+        the shared-stream layout lets same-session continuations skip their compares)."""
+        n = self.lin.astype(np.int64) + self.lout
+        off = np.zeros(self.n_requests, np.uint64)
+        off[1:] = np.cumsum(n)[:-1]
+        idx = np.concatenate([np.arange(int(o), int(o) + int(k), dtype=np.int64) for o, k in zip(self.off, n)]) \
+            if self.n_requests else np.zeros(0, np.int64)
+        return Trace(np.ascontiguousarray(self.tokens[idx]), off, self.lin.copy(), self.lout.copy(),
+                     self.name + "-copy", self.seed)
+
     def head(self, n: int) -> "Trace":
         """First n requests (the token pool is shared, unchanged)."""
         return Trace(self.tokens, self.off[:n].copy(), self.lin[:n].copy(),
@@ -475,10 +488,21 @@ GB = 1_000_000_000
 UNLIMITED_BYTES = (1 << 64) - 1   # "bytes unlimited" (toy config: node-count capacity only)
 
 
-def workload(cfg: int, R: Optional[int] = None, problem: int = 0) -> Workload:
+def workload(cfg: int, R: Optional[int] = None, problem: int = 0, layout: str = "stream") -> Workload:
     """Build config `cfg` (1..5).  R overrides the request count (for small parity runs).
     problem > 0 draws an independent trace of the same shape (seed offset), used by the
-    weak-scaling bench (one α-tuning problem per GPU)."""
+    weak-scaling bench (one α-tuning problem per GPU).  layout = "copy": every request
+    holds its own copy of its sequence (Trace.copy_layout)."""
+    w = _workload(cfg, R, problem)
+    if layout == "copy":
+        w.trace = w.trace.copy_layout()
+        w.name += "-copy"
+    elif layout != "stream":
+        raise ValueError(f"unknown layout {layout}")
+    return w
+
+
+def _workload(cfg: int, R: Optional[int], problem: int) -> Workload:
     seed = 1000 + cfg + 7919 * problem
     if cfg == 1:
         tr = toy_trace(seed, R or 16)
