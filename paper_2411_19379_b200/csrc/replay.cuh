@@ -113,9 +113,9 @@ struct DevSnapStore {
 // per snapshot at setup (image_kernel) so the 16+ chains that start from the same
 // snapshot copy it (coalesced, no child-index CAS, no Eq. 1 divisions) instead of
 // rebuilding it.  Byte layout from the image base (n = nodes):
-//   ImgHdr 64 | records 32(n+1) | ids 4(n+1) | dense 8(n+1) | exact eff 8(n+1) |
-//   child-index positions 4n | child-index entries 16n      (regions 16 B aligned)
-// (dense and eff are indexed by slot; slot 0, the root, is a hole)
+//   ImgHdr 64 | records 32(n+1) | dense 8(n+1) | child-index positions 4n |
+//   child-index entries 16n      (regions 16 B aligned)
+// (records carry the node ids; dense is indexed by slot; slot 0, the root, is a hole)
 struct ImgHdr {
   unsigned long long total;
   uint32_t n, nid, tmin, tmax;
@@ -124,10 +124,8 @@ struct ImgHdr {
   uint32_t bc_valid, pad0, pad1, pad2;
 };
 __host__ __device__ inline uint64_t img_al16(uint64_t x) { return (x + 15) & ~15ull; }
-__host__ __device__ inline uint64_t img_off_ids(uint32_t n) { return 64 + 32ull * (n + 1); }
-__host__ __device__ inline uint64_t img_off_dense(uint32_t n) { return img_off_ids(n) + img_al16(4ull * (n + 1)); }
-__host__ __device__ inline uint64_t img_off_eff(uint32_t n) { return img_off_dense(n) + img_al16(8ull * (n + 1)); }
-__host__ __device__ inline uint64_t img_off_tpos(uint32_t n) { return img_off_eff(n) + img_al16(8ull * (n + 1)); }
+__host__ __device__ inline uint64_t img_off_dense(uint32_t n) { return 64 + 32ull * (n + 1); }
+__host__ __device__ inline uint64_t img_off_tpos(uint32_t n) { return img_off_dense(n) + img_al16(8ull * (n + 1)); }
 __host__ __device__ inline uint64_t img_off_tent(uint32_t n) { return img_off_tpos(n) + img_al16(4ull * n); }
 __host__ __device__ inline uint64_t img_bytes(uint32_t n) { return img_off_tent(n) + 16ull * n; }
 // Writable view used by the live pass.
@@ -143,12 +141,13 @@ struct DevSnapOut {
 
 struct __align__(8) DenseRec {  // one dense position: the scanned key pair
   uint32_t tc;  // t_last | D_PIN | D_MULTI
-  float e32;    // RN32(eff) -- filter and bounds; the exact eff lives in WS::eff64
+  float e32;    // RN32(eff) -- filter and bounds; the exact eff is recomputed from the record
 };
 
 struct __align__(16) NodeRec {
   uint32_t parent, hidx, ds, de;  // hidx = position of the node's own entry in the child index
-  uint32_t roff, cxor, nf, pad;   // roff = pool offset of the node's request; nf = nchild | flags << 24
+  uint32_t roff, cxor, nf, id;    // roff = pool offset of the node's request; nf = nchild | flags << 24;
+                                  // id = creation ordinal (R4)
 };
 
 struct KParams {
@@ -188,15 +187,17 @@ struct KParams {
 // Per-worker workspace slice.  The caller zero-initialises the workspace once
 // (header word 0 = child-index generation, word 1 = layout signature).
 // Slice layout (byte offsets from the slice base; n = ncap, h = hcap):
-//   header 256 | records 32n | ids 4n | scratch 4n | path 4n | freel 4n | child index 16h |
-//   dense tail 8n | exact eff (f64) 8n
+//   header 256 | records 32n | scratch 4n | path 4n | freel 4n | child index 16h |
+//   dense tail 8n
 // (n is a power of two >= 64, so every region stays 16 B aligned).  ws_bytes_per_worker
 // is the end of the last region, so the accessors below and the stride cannot disagree.
-__host__ __device__ inline uint64_t ws_off_tab(uint32_t n) { return 256 + 48ull * n; }
+// Node ids live in the records and the exact fp64 eff is recomputed from a record when a
+// cold path needs it (one IEEE division, bit-identical to the value the dense list's
+// RN32 came from), so neither is a per-slot array a chain must copy or keep in L2.
+__host__ __device__ inline uint64_t ws_off_tab(uint32_t n) { return 256 + 44ull * n; }
 __host__ __device__ inline uint64_t ws_off_tail(uint32_t n, uint32_t h) { return ws_off_tab(n) + 16ull * h; }
-__host__ __device__ inline uint64_t ws_off_eff(uint32_t n, uint32_t h) { return ws_off_tail(n, h) + 8ull * n; }
 __host__ __device__ inline uint64_t ws_bytes_per_worker(uint32_t ncap, uint32_t hcap) {
-  const uint64_t b = ws_off_eff(ncap, hcap) + 8ull * ncap;
+  const uint64_t b = ws_off_tail(ncap, hcap) + 8ull * ncap;
   return (b + 255) & ~255ull;
 }
 
@@ -205,13 +206,11 @@ struct WS {
   uint32_t n, h;
   __device__ __forceinline__ uint32_t* hdr() const { return (uint32_t*)b; }
   __device__ __forceinline__ NodeRec* rec() const { return (NodeRec*)(b + 256); }
-  __device__ __forceinline__ uint32_t* ids() const { return (uint32_t*)(b + 256 + 32ull * n); }
-  __device__ __forceinline__ uint32_t* scratch() const { return (uint32_t*)(b + 256 + 36ull * n); }  // dump map
-  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 40ull * n); }
-  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 44ull * n); }
+  __device__ __forceinline__ uint32_t* scratch() const { return (uint32_t*)(b + 256 + 32ull * n); }  // dump map
+  __device__ __forceinline__ uint32_t* path() const { return (uint32_t*)(b + 256 + 36ull * n); }
+  __device__ __forceinline__ uint32_t* freel() const { return (uint32_t*)(b + 256 + 40ull * n); }
   __device__ __forceinline__ HEnt* tab() const { return (HEnt*)(b + ws_off_tab(n)); }
   __device__ __forceinline__ DenseRec* tail() const { return (DenseRec*)(b + ws_off_tail(n, h)); }
-  __device__ __forceinline__ double* eff64() const { return (double*)(b + ws_off_eff(n, h)); }
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -447,8 +446,14 @@ __device__ __forceinline__ void hash_erase_at_1(Chain& C, uint32_t i) {
 // ---- dense live list: positions < S in shared memory, the tail in global ----
 __device__ __forceinline__ DenseRec* d_ptr(const Chain& C, uint32_t i) { return i < C.S ? C.sd + i : C.w.tail() + i; }
 __device__ __forceinline__ uint32_t d_tc(const Chain& C, uint32_t i) { return d_ptr(C, i)->tc; }
-__device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return C.w.eff64()[i]; }
-__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.ids()[i]; }
+__device__ __forceinline__ double rec_eff(const DevModel& m, const NodeRec& R) {
+  return node_eff(m, R.ds, R.de, (R.nf >> 24) & F_SSM);
+}
+// out of line: the IEEE division sequence is long and the callers (a logged or near-tied
+// victim's exact utility) are cold
+__device__ __noinline__ double slot_eff(const NodeRec* rec, const DevModel m, uint32_t i) { return rec_eff(m, rec[i]); }
+__device__ __forceinline__ double d_eff(const Chain& C, uint32_t i) { return slot_eff(C.w.rec(), C.K->m, i); }
+__device__ __forceinline__ uint32_t d_id(const Chain& C, uint32_t i) { return C.w.rec()[i].id; }
 __device__ __forceinline__ void d_hole(Chain& C, uint32_t i) {
   DenseRec h;
   h.tc = HOLE_TC;
@@ -483,7 +488,6 @@ __device__ __forceinline__ void bc_remove(Chain& C, uint32_t t, float e) {
 }
 // eff of an EXISTING dense position changes
 __device__ __forceinline__ void d_set_eff(Chain& C, uint32_t i, double v) {
-  C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
   const float e = __double2float_rn(v);
   bc_change_e(C, d->e32, e, v);
@@ -504,7 +508,6 @@ __device__ __forceinline__ void dense_add_1(Chain& C, uint32_t s, uint32_t t) {
   C.count++;
   const NodeRec& R = C.w.rec()[s];
   const double v = node_eff(C.K->m, R.ds, R.de, (R.nf >> 24) & F_SSM);
-  C.w.eff64()[i] = v;
   DenseRec* d = d_ptr(C, i);
   d->e32 = __double2float_rn(v);
   d->tc = t | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
@@ -585,7 +588,7 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
   __syncwarp();
   if (lane == 0) {
     NodeRec z;
-    z.parent = NIL; z.hidx = NIL; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.pad = 0;
+    z.parent = NIL; z.hidx = NIL; z.ds = 0; z.de = 0; z.roff = 0; z.cxor = 0; z.nf = 0; z.id = 0;
     C.w.rec()[0] = z;
     d_hole(C, 0);  // the root is never a candidate and not in the bounds
   }
@@ -605,9 +608,8 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     R.roff = (uint32_t)r.ref_off;
     R.cxor = 0;
     R.nf = (r.has_ssm ? F_SSM : 0u) << 24;
-    R.pad = 0;
+    R.id = r.id;
     C.w.rec()[s] = R;
-    C.w.ids()[s] = r.id;
     bytes += node_bytes(C.K->m, r.d_start, r.d_end, r.has_ssm);
   }
   __syncwarp();
@@ -638,7 +640,6 @@ __device__ void load_snapshot(Chain& C, const KParams& P, const DevSnapStore* st
     const uint32_t s = i + 1;
     const NodeRec R = C.w.rec()[s];
     const double v = node_eff(C.K->m, R.ds, R.de, (R.nf >> 24) & F_SSM);
-    C.w.eff64()[s] = v;
     DenseRec* d = d_ptr(C, s);
     d->tc = nodes[i].t_last | ((R.nf & NCH_MASK) >= C.mthr ? D_MULTI : 0u);
     // vLLM+ keeps the node id in the second dense word (LRU key (t, id)); Marconi RN32(eff)
@@ -673,7 +674,6 @@ __device__ void export_image(Chain& C, char* dst) {
   float lo = __int_as_float(0x7F800000), hi = 0.0f;
   double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
   const DenseRec* dense = C.w.tail();
-  const double* e64 = C.w.eff64();
   for (uint32_t i = lane + 1; i <= n; i += 32) {  // slots 1..n (slot 0 = root hole)
     const DenseRec d = dense[i];
     const uint32_t t = d.tc & T_MASK;
@@ -681,7 +681,7 @@ __device__ void export_image(Chain& C, char* dst) {
     tmx = max(tmx, t);
     lo = fminf(lo, d.e32);
     hi = fmaxf(hi, d.e32);
-    const double e = e64[i];
+    const double e = d_eff(C, i);
     elo = e < elo ? e : elo;
     ehi = e > ehi ? e : ehi;
   }
@@ -695,16 +695,12 @@ __device__ void export_image(Chain& C, char* dst) {
     elo = a < elo ? a : elo;
     ehi = b > ehi ? b : ehi;
   }
-  // records, ids, dense, eff (all by slot)
+  // records (with ids) and dense, by slot
   NodeRec* rec = (NodeRec*)(dst + 64);
-  uint32_t* ids = (uint32_t*)(dst + img_off_ids(n));
   DenseRec* dn = (DenseRec*)(dst + img_off_dense(n));
-  double* ef = (double*)(dst + img_off_eff(n));
   for (uint32_t i = lane; i <= n; i += 32) {
     rec[i] = C.w.rec()[i];
-    ids[i] = C.w.ids()[i];
     dn[i] = dense[i];
-    ef[i] = (i == 0) ? 0.0 : e64[i];
   }
   // occupied child-index slots of this generation, compacted in slot order
   uint32_t* tpos = (uint32_t*)(dst + img_off_tpos(n));
@@ -801,10 +797,7 @@ __device__ __forceinline__ void warp_copy16(uint4* __restrict__ d, const uint4* 
 __device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S, const char* __restrict__ src,
                                         uint32_t n, uint32_t g) {
   const uint32_t lane = lane_id();
-  // records + ids are contiguous in the image but not in the slice
   warp_copy16((uint4*)w.rec(), (const uint4*)(src + 64), 2 * (n + 1));
-  warp_copy16((uint4*)w.ids(), (const uint4*)(src + img_off_ids(n)), (uint32_t)(img_al16(4ull * (n + 1)) / 16));
-  warp_copy16((uint4*)w.eff64(), (const uint4*)(src + img_off_eff(n)), (n + 2) / 2);
   // dense list: the shared-memory part [0, ns) by one bulk copy on the TMA engine (its
   // 16-byte multiple; an odd last entry by lane 0) while the warp copies the rest; the
   // copy completes on the warp's mbarrier (at sd + S + 12, its phase word beside it)
@@ -916,8 +909,8 @@ __device__ void dump_snapshot(Chain& C, const KParams& P, DevSnapOut* out, uint3
     const NodeRec R = C.w.rec()[s];
     const uint32_t p = R.parent;
     mc_snap_node r;
-    r.id = C.w.ids()[s];
-    r.parent_id = (p == 0) ? 0u : C.w.ids()[p];
+    r.id = R.id;
+    r.parent_id = (p == 0) ? 0u : C.w.rec()[p].id;
     r.ref_off = R.roff;
     r.d_start = R.ds;
     r.d_end = R.de;
@@ -1022,14 +1015,18 @@ __device__ __forceinline__ void scan_dense(const Chain& C, uint32_t cnt, F&& f) 
 }
 
 // Cold paths of the victim selection, kept out of line (instruction cache).
-__device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const DenseRec* tail, const double* e64,
-                                                 uint32_t cnt, uint32_t S, float lo32, float hi32) {
+// (rec, m: the exact eff of a slot is recomputed from its record, rec_eff)
+__device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const DenseRec* tail, const NodeRec* rec,
+                                                 const DevModel m, uint32_t cnt, uint32_t S, float lo32, float hi32) {
   const uint32_t lane = lane_id();
   double elo = __longlong_as_double(0x7FF0000000000000ll), ehi = 0.0;
   for (uint32_t i = lane; i < cnt; i += 32) {
     const float e = (i < S ? sd[i] : tail[i]).e32;
-    if (e == lo32) elo = fmin(elo, e64[i]);
-    if (e == hi32) ehi = fmax(ehi, e64[i]);
+    if (e == lo32 || e == hi32) {
+      const double x = rec_eff(m, rec[i]);
+      if (e == lo32) elo = fmin(elo, x);
+      if (e == hi32) ehi = fmax(ehi, x);
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -1039,16 +1036,17 @@ __device__ __noinline__ double2 recover_extremes(const DenseRec* sd, const Dense
   }
   return make_double2(elo, ehi);
 }
-__device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* tail, const double* e64,
-                                          const uint32_t* ids, uint32_t cnt, uint32_t S, Bounds b, double alpha) {
+__device__ __noinline__ Best exact_select(const DenseRec* sd, const DenseRec* tail, const NodeRec* rec,
+                                          const DevModel m, uint32_t cnt, uint32_t S, Bounds b, double alpha) {
   const uint32_t lane = lane_id();
   Best best;
   best_init(best);
   for (uint32_t i = lane; i < cnt; i += 32) {
     const uint32_t tc = (i < S ? sd[i] : tail[i]).tc;
     if (tc & D_FLAGS) continue;
-    const double u = utility(b, tc, e64[i], alpha);
-    const uint32_t id = ids[i];
+    const NodeRec R = rec[i];
+    const double u = utility(b, tc, rec_eff(m, R), alpha);
+    const uint32_t id = R.id;
     if (best.i == NIL || better(u, tc, id, best)) {
       best.u = u; best.t = tc; best.id = id; best.i = i;
     }
@@ -1098,14 +1096,14 @@ __device__ __noinline__ Bounds32 bounds_pass(const DenseRec* sd, const DenseRec*
 }
 
 // α = 0 with the oldest t shared by several candidates: the one with the smallest id.
-__device__ __noinline__ uint32_t lru_tiebreak(const DenseRec* sd, const DenseRec* tail, const uint32_t* ids,
+__device__ __noinline__ uint32_t lru_tiebreak(const DenseRec* sd, const DenseRec* tail, const NodeRec* rec,
                                               uint32_t cnt, uint32_t S, uint32_t t) {
   const uint32_t lane = lane_id();
   uint32_t bid = 0xFFFFFFFFu, bi = NIL;
   for (uint32_t i = lane; i < cnt; i += 32) {
     const uint32_t tc = (i < S ? sd[i] : tail[i]).tc;
     if (!(tc & D_FLAGS) && tc == t) {
-      const uint32_t id = ids[i];
+      const uint32_t id = rec[i].id;
       if (id < bid) { bid = id; bi = i; }
     }
   }
@@ -1173,7 +1171,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     if (unique) {
       best.i = __shfl_sync(FULL, i1, __ffs(at) - 1);
     } else {  // several candidates share the oldest t: smallest id (R4), cold path
-      best.i = lru_tiebreak(C.sd, C.w.tail(), C.w.ids(), cnt, C.S, tbest);
+      best.i = lru_tiebreak(C.sd, C.w.tail(), C.w.rec(), cnt, C.S, tbest);
     }
     best.slot = best.i;
     const double rec = (b.tmax == b.tmin) ? 0.5 : __ddiv_rn((double)(best.t - b.tmin), (double)(b.tmax - b.tmin));
@@ -1214,7 +1212,6 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   const float idt = dt0 ? 0.0f : __frcp_rn((float)(tmax - tmin));
   const float aide = (de32 == 0.0) ? 0.0f : __double2float_rn(__ddiv_rn(C.K->alpha, de32));
   const float INF = __int_as_float(0x7F800000);
-  const double* __restrict__ e64 = C.w.eff64();
   float a1[kUnroll], a2[kUnroll];
   uint32_t ai[kUnroll];
 #pragma unroll
@@ -1242,7 +1239,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
 #define ENSURE_EXTREMES()                                                                  \
   do {                                                                                     \
     if ((C.bc_valid & 6u) != 6u) {                                                         \
-      const double2 ex = recover_extremes(C.sd, C.w.tail(), e64, cnt, C.S, lo32, hi32);    \
+      const double2 ex = recover_extremes(C.sd, C.w.tail(), C.w.rec(), C.K->m, cnt, C.S, lo32, hi32); \
       Cw.bc_elo = ex.x; Cw.bc_ehi = ex.y; Cw.bc_valid |= 6u;                               \
     }                                                                                      \
     b.emin = C.bc_elo; b.emax = C.bc_ehi;                                                  \
@@ -1252,7 +1249,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   // comparisons): the exact fp64 pass decides, as the oracle does for any finite α.
   if (!(kmin < INF)) {
     ENSURE_EXTREMES();
-    return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.K->alpha);
+    return exact_select(C.sd, C.w.tail(), C.w.rec(), C.K->m, cnt, C.S, b, C.K->alpha);
   }
   // δ = 2^-19 (1 + α (1 + 4 emax/Δe32)); a zero fp32 range cannot resolve eff -> exact pass
   if (de32 == 0.0) ENSURE_EXTREMES();
@@ -1270,7 +1267,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
       best.id = NIL;
       if (need_u) {  // the exact utility is only logged (no global read otherwise)
         ENSURE_EXTREMES();
-        if (mine) best.u = utility(b, d_tc(C, i1), e64[i1], C.K->alpha);
+        if (mine) best.u = utility(b, d_tc(C, i1), d_eff(C, i1), C.K->alpha);
         best.u = __shfl_sync(FULL, best.u, src);
       }
       return best;
@@ -1281,7 +1278,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
     ENSURE_EXTREMES();
     if (mine) {  // near-ties: exact utilities, ids for exact ties
       best.t = d_tc(C, i1);
-      best.u = utility(b, best.t, e64[i1], C.K->alpha);
+      best.u = utility(b, best.t, d_eff(C, i1), C.K->alpha);
       best.i = i1;
       best.slot = i1;
       best.id = d_id(C, i1);
@@ -1295,7 +1292,7 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   // near-ties / unresolvable fp32 range: exact full pass (cold path)
   ENSURE_EXTREMES();
 #undef ENSURE_EXTREMES
-  return exact_select(C.sd, C.w.tail(), e64, C.w.ids(), cnt, C.S, b, C.K->alpha);
+  return exact_select(C.sd, C.w.tail(), C.w.rec(), C.K->m, cnt, C.S, b, C.K->alpha);
 }
 
 __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* log, uint32_t* log_n) {
@@ -1324,7 +1321,7 @@ __device__ void evict_one(Chain& C, const KParams& P, uint32_t r, mc_evict_rec* 
     const uint32_t p = X.parent;
     const uint32_t xf = X.nf >> 24;
     const NodeRec Rp = C.w.rec()[p];
-    const uint32_t xid = log ? C.w.ids()[x] : 0u;
+    const uint32_t xid = X.id;
     const DenseRec dv = *d_ptr(C, x);
     uint32_t kind;
     if ((X.nf & NCH_MASK) == 0) {  // leaf: free KVs + state
@@ -1390,9 +1387,8 @@ __device__ __forceinline__ uint32_t split_1(Chain& C, const KParams& P, uint32_t
   const uint32_t ytok = C.w.tab()[hi].tok;
   NodeRec U;
   U.parent = Y.parent; U.hidx = hi; U.ds = Y.ds; U.de = x;
-  U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.pad = 0;
+  U.roff = Y.roff; U.cxor = y; U.nf = 1u | ((stateful ? F_SSM : 0u) << 24); U.id = C.next_id++;
   C.w.rec()[u] = U;
-  C.w.ids()[u] = C.next_id++;
   C.w.tab()[hi] = hmake(C, Y.parent, ytok, u, x, stateful, Y.roff);  // same key, new child
   NodeRec& Ry = C.w.rec()[y];
   Ry.parent = u;
@@ -1653,9 +1649,8 @@ __device__ ReqOut process_request(Chain& C, const KParams& P, uint32_t r, const 
           const NodeRec Ra = C.w.rec()[attach];
           NodeRec W;
           W.parent = attach; W.hidx = NIL; W.ds = m; W.de = n;
-          W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.pad = 0;
+          W.roff = (uint32_t)off; W.cxor = 0; W.nf = F_SSM << 24; W.id = C.next_id++;
           C.w.rec()[w] = W;
-          C.w.ids()[w] = C.next_id++;
           C.w.rec()[w].hidx = hash_insert_1(C, hmake(C, attach, ft, w, n, true, (uint32_t)off), attach);
           NodeRec& Wa = C.w.rec()[attach];
           Wa.nf = Ra.nf + 1;
@@ -1966,7 +1961,7 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           R.roff = (uint32_t)off;
           R.cxor = inner ? path[k + 1] : 0u;
           R.nf = (F_SSM << 24) | (inner ? 1u : 0u);
-          R.pad = 0;
+          R.id = id0 + j;
           const uint32_t h = block_hash_1(P.tok + off + (uint64_t)k * x, x);
           uint32_t hi = hslot(par, h, C.hmask);
           const uint32_t nk = hkey(C, par, s);
@@ -1981,7 +1976,6 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
           E.roff = R.roff;
           R.hidx = hi;
           C.w.rec()[s] = R;
-          C.w.ids()[s] = id0 + j;
           DenseRec* d = d_ptr(C, s);
           d->tc = r | (inner ? D_MULTI : 0u);
           d->e32 = __uint_as_float(id0 + j);  // vLLM+: the id, so (t, id) LRU keys need no global read
