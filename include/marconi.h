@@ -183,6 +183,13 @@ mc_status mc_live_pass_bootstrap(mc_ctx* ctx, uint32_t multiplier, void* d_works
                                  uint32_t* d_hit, uint64_t* d_flops, uint8_t* d_bypass, uint32_t* h_first_evict,
                                  void* stream);
 
+/* SM cycles the last live pass (mc_live_pass / mc_live_pass_at) spent on each window
+ * between consecutive snapshot points of `variant` (window k = requests after point k
+ * up to point k+1, the last one to the end of the trace) -- the α = 0 cost of segment k,
+ * which grid.AlphaGrid uses to order chains longest-first.  h_out (host, nullable) gets
+ * *n_out = number of points values. */
+mc_status mc_live_window_cycles(mc_ctx* ctx, uint32_t variant, uint64_t* h_out, uint32_t cap, uint32_t* n_out);
+
 /* Number of snapshots held for a variant and copy one back as canonical
  * records sorted by id (host).  *n_out receives the record count; h_out may be
  * NULL to query it. */

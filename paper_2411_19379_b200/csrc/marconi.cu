@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   DevSnapOut* out = P.live_out + v;
   dump_snapshot(C, P, out, 0);
   uint32_t next = 1, first = 0, boot_end = 0;
+  long long tw = clock64();  // start of the current window (chain-cost feedback for the α-grid)
   Prefetched cur = fetch_request(P, 1), nxt = cur;
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
     const uint32_t ev0 = C.n_evict;
@@ -202,12 +203,19 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
       if (r == boot_end && r < P.n_req) dump_snapshot(C, P, out, 2);
     } else {
       while (next < P.n_points && P.live_points[next] == r) {
+        if (lane == 0 && P.live_cyc) {
+          const long long now = clock64();
+          P.live_cyc[(uint64_t)v * P.n_points + next - 1] = (unsigned long long)(now - tw);
+          tw = now;
+        }
         dump_snapshot(C, P, out, next);
         next++;
       }
     }
   }
   if (lane == 0 && P.first_evict) P.first_evict[v] = first;
+  if (lane == 0 && P.live_cyc && !P.live_mult)  // the last window (after the last point)
+    P.live_cyc[(uint64_t)v * P.n_points + P.n_points - 1] = (unsigned long long)(clock64() - tw);
 }
 
 // Device-side trace check (mc_set_trace_async): the same rules as mc_set_trace's host
@@ -330,6 +338,8 @@ struct mc_ctx {
   mc_segment* d_segs = nullptr;
   uint32_t* d_status = nullptr;
   uint32_t* d_points = nullptr;  // live-pass snapshot points + first-eviction outputs
+  unsigned long long* d_live_cyc = nullptr;  // [n_var][points] cycles per live-pass window
+  uint32_t live_points = 0;
   uint32_t alpha_cap = 0;        // α values per mc_replay call (they travel in the workspace header)
   char* img_scratch = nullptr;   // image_kernel workspace slices (zeroed once, reused: generation tags)
   uint64_t img_scratch_bytes = 0;
@@ -554,6 +564,7 @@ void mc_destroy(mc_ctx* c) {
   cudaFree(c->d_segs);
   cudaFree(c->d_status);
   cudaFree(c->d_points);
+  cudaFree(c->d_live_cyc);
   delete c;
 }
 
@@ -728,7 +739,12 @@ mc_status live_pass_impl(mc_ctx* c, const uint32_t* h_points, uint32_t n_points,
   }
   cudaFree(c->d_points);
   c->d_points = nullptr;
+  cudaFree(c->d_live_cyc);
+  c->d_live_cyc = nullptr;
   CU(cudaMalloc(&c->d_points, sizeof(uint32_t) * (K + nv)));
+  CU(cudaMalloc(&c->d_live_cyc, sizeof(unsigned long long) * K * nv));
+  CU(cudaMemsetAsync(c->d_live_cyc, 0, sizeof(unsigned long long) * K * nv, (cudaStream_t)stream));
+  c->live_points = K;
   cudaStream_t st = (cudaStream_t)stream;
   DevSnapOut* d_outs = (DevSnapOut*)((char*)d_ws + 256);
   if (sizeof(DevSnapOut) * nv + 256 > kCtrl) return fail(MC_EINVAL, "too many variants for the live pass");
@@ -766,6 +782,7 @@ mc_status live_pass_impl(mc_ctx* c, const uint32_t* h_points, uint32_t n_points,
   P.n_points = K;
   P.first_evict = c->d_points + K;
   P.live_mult = mult;
+  P.live_cyc = c->d_live_cyc;
   P.smem_nodes = c->smem_nodes_live;
   live_kernel<<<nv, 32, 8ull * c->smem_nodes_live, st>>>(P);
   CU(cudaGetLastError());
@@ -815,6 +832,18 @@ mc_status mc_live_pass(mc_ctx* c, uint32_t window, void* d_ws, uint64_t ws_bytes
 mc_status mc_snapshot_count(const mc_ctx* c, uint32_t variant, uint32_t* n_out) {
   if (!c || !n_out || variant >= c->hv.size()) return fail(MC_EINVAL, "mc_snapshot_count: bad argument");
   *n_out = c->snaps[variant].count;
+  return MC_OK;
+}
+
+mc_status mc_live_window_cycles(mc_ctx* c, uint32_t variant, uint64_t* h_out, uint32_t cap, uint32_t* n_out) {
+  if (!c || !n_out || variant >= c->hv.size()) return fail(MC_EINVAL, "mc_live_window_cycles: bad argument");
+  if (!c->d_live_cyc) return fail(MC_ESTATE, "mc_live_window_cycles before a live pass");
+  *n_out = c->live_points;
+  if (!h_out) return MC_OK;
+  if (cap < c->live_points) return fail(MC_EINVAL, "output buffer too small");
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(h_out, c->d_live_cyc + (uint64_t)variant * c->live_points, sizeof(uint64_t) * c->live_points,
+                cudaMemcpyDeviceToHost));
   return MC_OK;
 }
 

@@ -181,6 +181,7 @@ struct KParams {
   uint32_t n_points;
   uint32_t* first_evict;        // [n_var] first request whose admission evicted (0 = none)
   uint32_t live_mult;           // > 0: bootstrap points instead (snapshot 1 after r_F, 2 after r_F + mult r_F)
+  unsigned long long* live_cyc; // [n_var][n_points] SM cycles the live pass spent on window k (static points)
   uint32_t smem_nodes;  // dense positions held in shared memory per warp
 };
 

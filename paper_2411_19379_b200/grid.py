@@ -29,6 +29,15 @@ def chain_costs(lens: np.ndarray, segs, n_var: int, n_alpha: int) -> np.ndarray:
     return np.tile(seg_cost, n_var * n_alpha)
 
 
+def chain_costs_live(window_cycles: Sequence[np.ndarray], segs, n_alpha: int) -> np.ndarray:
+    """Cost per chain id from the α = 0 live pass: the device cycles it spent on the
+    segment's window (mc_live_window_cycles; the same requests from the same tree at α = 0),
+    for every α of the segment.  Chains are independent, so only the order changes."""
+    per_vs = np.asarray([[int(wc[k]) if k < len(wc) else 0 for (_, _, k) in segs] for wc in window_cycles],
+                        np.int64)                                   # [variant, segment]
+    return np.repeat(per_vs, n_alpha, axis=0).reshape(-1)           # chain id = (v * n_alpha + a) * ns + s
+
+
 def lpt_shard(costs: np.ndarray, n_segs: int, n_alpha: int, world: int) -> List[np.ndarray]:
     """Deterministic longest-processing-time assignment of chains to ranks.
 
@@ -126,8 +135,12 @@ class AlphaGrid:
                 self.ctx.set_snapshots(v, snaps)
             self.live = None
         self.ctx.set_segments(self.segs)
-        lens = tr.lin.astype(np.int64) + tr.lout
-        costs = chain_costs(lens, self.segs, len(self.variants), len(self.alphas))
+        if self.live is not None:  # longest chains first: the live pass's own window cycles
+            costs = chain_costs_live([self.ctx.live_window_cycles(v) for v in range(len(self.variants))],
+                                     self.segs, len(self.alphas))
+        else:
+            lens = tr.lin.astype(np.int64) + tr.lout
+            costs = chain_costs(lens, self.segs, len(self.variants), len(self.alphas))
         self.shards = lpt_shard(costs, len(self.segs), len(self.alphas), self.world)
         self.chains = self.shards[self.rank]
         dflt = self.ctx.workspace_size(0, len(self.alphas), len(self.chains))
@@ -143,6 +156,14 @@ class AlphaGrid:
 
     def run(self, out=None, **kw):
         return self.ctx.replay(self.alphas, chains=self.chains, workspace=self.workspace, out=out, **kw)
+
+    def reorder_by_cycles(self, cycles) -> None:
+        """Cost feedback: order this rank's chains longest-first by the per-chain cycles a
+        previous replay of the same chains measured (outputs["cycles"]); the persistent
+        queue then packs them LPT.  Results never depend on the order."""
+        cyc = np.asarray(cycles.cpu().numpy() if hasattr(cycles, "cpu") else cycles, np.int64)
+        ch = self.chains.astype(np.int64)
+        self.chains = ch[np.lexsort((ch, -cyc[ch]))].astype(np.uint32)
 
     def select(self, out, gathered=None) -> List[float]:
         hs = gathered if gathered is not None else gather_hit_sums(out["hit_sum"], self.world, self.group)

@@ -26,7 +26,7 @@ EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n
 assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
 
 EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at", "mc_live_pass_bootstrap",
-            "mc_snapshot_count",
+            "mc_snapshot_count", "mc_live_window_cycles",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
             "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log")
 
@@ -80,6 +80,7 @@ def lib():
             "mc_live_pass_at": [P, P, U32, P, U64, P, P, P, P, P],
             "mc_live_pass_bootstrap": [P, U32, P, U64, P, P, P, P, P],
             "mc_snapshot_count": [P, U32, P],
+            "mc_live_window_cycles": [P, U32, P, U32, P],
             "mc_get_snapshot": [P, U32, U32, P, U64, P, P],
             "mc_set_segments": [P, P, U32],
             "mc_workspace_size": [P, U32, U32, U32, P],
@@ -227,6 +228,14 @@ class Context:
         n = C.c_uint32()
         check(lib().mc_snapshot_count(self.h, variant, C.byref(n)))
         return n.value
+
+    def live_window_cycles(self, variant: int) -> np.ndarray:
+        """Cycles the last live pass spent per window between its snapshot points (u64)."""
+        n = C.c_uint32()
+        check(lib().mc_live_window_cycles(self.h, variant, None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        check(lib().mc_live_window_cycles(self.h, variant, _np_ptr(out), n.value, C.byref(n)))
+        return out
 
     def get_snapshot(self, variant: int, k: int):
         n = C.c_uint64()

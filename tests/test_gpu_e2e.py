@@ -100,3 +100,24 @@ def test_async_trace_check_length_limit():
         else:
             with pytest.raises(M.MarconiError, match="request 2 "):
                 ctx.check()
+
+
+def test_cost_feedback_order_changes_no_result():
+    """Chains ordered by the live pass's window cycles, then re-ordered by the measured
+    per-chain cycles of a replay (grid.AlphaGrid.reorder_by_cycles): the same chain set,
+    identical per-request hits, FLOPs and hit sums."""
+    w = tg.workload(5, R=8000)
+    g = AlphaGrid(w.trace, w.variants[:3], w.alphas[:4], w.n_segments).setup()
+    wc = g.ctx.live_window_cycles(0)
+    assert wc.shape[0] == w.n_segments and int(wc.sum()) > 0
+    out = g.run(chain_cycles=True)
+    g.ctx.check()
+    before = sorted(g.chains.tolist())
+    g.reorder_by_cycles(out["cycles"])
+    assert sorted(g.chains.tolist()) == before
+    cyc = out["cycles"].cpu().numpy()[g.chains.astype(np.int64)]
+    assert np.all(cyc[:-1] >= cyc[1:])  # longest first
+    out2 = g.run(chain_cycles=True)
+    g.ctx.check()
+    for k in ("hit", "flops", "bypass", "hit_sum"):
+        assert torch.equal(out[k], out2[k]), k
