@@ -839,7 +839,10 @@ __device__ __forceinline__ void copy_image(const WS w, DenseRec* sd, uint32_t S,
     }
   }
   ph = __shfl_sync(FULL, ph, 0);
-  if (nb) mbar_wait(bar, ph);
+  if (nb) {
+    mbar_wait(bar, ph);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // async-proxy writes before generic reads
+  }
 }
 
 // A chain's initial state from a snapshot image (replaces load_snapshot on the replay
