@@ -271,8 +271,8 @@ def main():
     t_gen = time.perf_counter() - t_gen
     w = ws[0]
     tr = w.trace
-    pol = (f"vLLM+ baseline (state per token block, LRU; blocks {args.blocks} x caches {args.caps_gb} GB), "
-           if args.policy == "vllm" else "")
+    pol = (f"vLLM+ baseline (state per token block, full blocks only as in vLLM, LRU; blocks {args.blocks} x "
+           f"caches {args.caps_gb} GB), " if args.policy == "vllm" else "")
     config = {"workload": f"config{args.config} {w.name}-shaped trace, {pol}{tr.n_requests} requests, "
                           f"{len(w.variants)} cache variant(s), {len(w.alphas)} alphas x {len(w.segments())} "
                           f"segments = {w.n_chains} chains" +
