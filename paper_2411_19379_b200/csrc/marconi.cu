@@ -50,7 +50,9 @@ constexpr int kWarpsPerCta = MC_WARPS_PER_CTA;
 // ---------------------------------------------------------------------------
 // kPolicy 0 = Marconi chains, 1 = vLLM+ chains (block_size > 0): one instantiation per
 // policy so the Marconi kernel carries no vLLM+ code (registers, instruction cache).
-template <int kPolicy>
+// kGen (Marconi chains): false = the lean instantiation (no eviction log, no chunked
+// checkpoints, n_ssm > 0), chosen by mc_replay whenever the call allows it.
+template <int kPolicy, bool kGen>
 #ifdef MC_MAXNREG  // explicit register budget (sizes the resident warps per SM instead of MC_MINBLOCKS)
 __global__ void __maxnreg__(MC_MAXNREG) replay_kernel(KParams P) {
 #else
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, MC_MINBLOCKS) replay_kernel
     for (uint32_t i = 0; i < seg.n_req && !C.failed; i++) {
       const uint32_t r = seg.first_req + i;
       const ReqOut o = kPolicy ? process_request_vllm(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n)
-                               : process_request(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n);
+                               : process_request<kGen>(C, P, r, cur, nxt, i + 1 < seg.n_req, log, log_n);
       cur = nxt;
       if (lane == 0) {
         P.hit[obase + r - 1] = o.reuse;
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
   for (uint32_t r = 1; r <= P.n_req && !C.failed; r++) {
     const uint32_t ev0 = C.n_evict;
     const ReqOut o = C.block ? process_request_vllm(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr)
-                             : process_request(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
+                             : process_request<true>(C, P, r, cur, nxt, r < P.n_req, nullptr, nullptr);
     cur = nxt;
     if (first == 0 && C.n_evict != ev0) {  // the paper's "first eviction"
       first = r;
@@ -513,11 +515,12 @@ mc_status mc_create(const mc_variant* hv, uint32_t n_var, uint32_t max_nodes, in
     c->smem_nodes = std::min<uint32_t>(c->smem_nodes, max_nodes);
     c->smem_nodes_live = std::min<uint32_t>((uint32_t)((smem_optin / 8) & ~31), max_nodes);
   }
-  cudaFuncSetAttribute(replay_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-  cudaFuncSetAttribute(replay_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(replay_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(replay_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  cudaFuncSetAttribute(replay_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   cudaFuncSetAttribute(live_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel<0>, 32 * kWarpsPerCta,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, replay_kernel<0, true>, 32 * kWarpsPerCta,
                                                 kWarpsPerCta * 8ull * c->smem_nodes);
   c->blocks_per_sm = std::max(1, bps);
   c->ncap = max_nodes;
@@ -963,6 +966,11 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
   if (kWarpsPerCta * 8ull * S > c->smem_optin) return fail(MC_EINVAL, "smem_nodes exceeds shared memory");
   if (S < 32) return fail(MC_EINVAL, "smem_nodes must be >= 32 (14 slots hold the chain counters, constants and the copy mbarrier)");
   P.smem_nodes = S;
+  // the lean Marconi instantiation unless this call logs evictions or a Marconi variant
+  // uses chunked checkpoints or has no SSM layers
+  bool lean = A->d_log == nullptr;
+  for (const auto& v : c->hv)
+    if (v.block_size == 0 && (v.chunk_size != 0 || v.model.n_ssm == 0)) lean = false;
   // one launch per policy group, back to back on `st` (they share the worker slices);
   // each launch has its own queue word
   const uint32_t groups[2] = {n_marconi, n_chains - n_marconi};
@@ -974,10 +982,12 @@ mc_status mc_replay(mc_ctx* c, const mc_replay_args* A, void* stream) {
     P.queue = (unsigned*)ws + 16 * g;
     P.n_workers = std::min(workers, groups[g]);
     const uint32_t ctas = (P.n_workers + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (g == 0)
-      replay_kernel<0><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
+    if (g == 0 && lean)
+      replay_kernel<0, false><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
+    else if (g == 0)
+      replay_kernel<0, true><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
     else
-      replay_kernel<1><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
+      replay_kernel<1, true><<<ctas, 32 * kWarpsPerCta, kWarpsPerCta * 8ull * S, st>>>(P);
     CU(cudaGetLastError());
     first += groups[g];
   }
