@@ -347,13 +347,11 @@ __device__ __forceinline__ void sync_state(Chain& C) {
 }
 
 __device__ __forceinline__ uint32_t hslot(uint32_t parent, uint32_t tok, uint32_t mask) {
-  unsigned long long key = ((unsigned long long)parent << 32) | tok;
-  key ^= key >> 33;
-  key *= 0xff51afd7ed558ccdull;
-  key ^= key >> 33;
-  key *= 0xc4ceb9fe1a85ec53ull;
-  key ^= key >> 33;
-  return (uint32_t)key & mask;
+  uint32_t h = tok * 0x9E3779B1u ^ parent * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 13;
+  return h & mask;
 }
 __device__ __forceinline__ bool hvalid(const Chain& C, uint32_t key) { return (key >> 28) == C.gen; }
 __device__ __forceinline__ uint32_t hkey(const Chain& C, uint32_t parent, uint32_t slot) {
