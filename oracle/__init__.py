@@ -18,6 +18,9 @@ Parity status of each function:
   counters (d.3 algorithmic bytes)                       pinned: the flat-list simulator's own
                                                           counts (tests/flatlist.py) + S1 by hand
   live_pass (segment snapshots)                          pinned: as Oracle.run + dump round-trip
+  Oracle.lookup (steps 1-4, read-only)                   pinned: the flat-list simulator's own lookup
+                                                          (tests/flatlist.py FlatCache.lookup) and
+                                                          the next step's hit
 """
 from __future__ import annotations
 
@@ -41,7 +44,9 @@ NODE_DTYPE = np.dtype([("id", "<u4"), ("parent_id", "<u4"), ("ref_off", "<u8"), 
                        ("d_end", "<u4"), ("t_last", "<u4"), ("has_ssm", "<u4")], align=True)
 EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n_live", "<u4"),
                         ("utility", "<f8")], align=True)
-assert NODE_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
+LOOKUP_DTYPE = np.dtype([("reuse", "<u4"), ("m", "<u4"), ("p", "<u4"), ("hit_id", "<u4"), ("div_id", "<u4"),
+                         ("div_off", "<u4"), ("path_len", "<u4"), ("d_nodes", "<u4"), ("d_bytes", "<u8")])
+assert NODE_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24 and LOOKUP_DTYPE.itemsize == 40
 
 
 def lib():
@@ -63,6 +68,7 @@ def lib():
         L.orc_dump.argtypes = [P, P, U64, P, P]
         L.orc_log.argtypes = [P, P, U64, P]
         L.orc_counters.argtypes = [P, P]
+        L.orc_lookup_req.argtypes = [P, U32, P]
         L.orc_total.argtypes = [P, P, P]
         L.orc_prefill_flops.argtypes = [P, U64, P]
         L.orc_layer_terms.argtypes = [P, U64, P]
@@ -178,6 +184,13 @@ class Oracle:
         b = np.zeros(1, np.uint32)
         _check(lib().orc_step(self.h, r, _ptr(h), _ptr(f), _ptr(b)))
         return int(h[0]), int(f[0]), int(b[0])
+
+    def lookup(self, r: int) -> np.ndarray:
+        """Steps 1-4 of c.2 for request r against the current tree, without mutating it:
+        one LOOKUP_DTYPE record (reuse, m, p, hit / divergence node, plan)."""
+        out = np.zeros(1, LOOKUP_DTYPE)
+        _check(lib().orc_lookup_req(self.h, r, _ptr(out)))
+        return out[0]
 
     def run(self, first: int, n: int):
         """Replay requests first..first+n-1 -> (hit u32[n], flops u64[n], bypass u32[n])."""

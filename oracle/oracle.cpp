@@ -52,6 +52,19 @@ struct orc_node {
   u32 t_last;
   u32 has_ssm;
 };
+// Read-only lookup of one request against the current tree (SURVEY.md §8(a) a2/a3 as a
+// standalone query, VERDICT r1 "mc_lookup"): steps 1-4 of c.2 without any mutation.
+struct orc_lookup {
+  u32 reuse;     // skipped prefill tokens (step 2)
+  u32 m;         // matched length of the full sequence (step 1)
+  u32 p;         // speculative-insertion checkpoint position after chunk alignment, 0 = none (step 3)
+  u32 hit_id;    // node whose state is reused (0 = none)
+  u32 div_id;    // node where the walk stopped: the mid-edge node, else the last full match (0 = root)
+  u32 div_off;   // m - d_start(div node): tokens of its edge that matched
+  u32 path_len;  // |P|: fully matched nodes + the partially matched one
+  u32 d_nodes;   // nodes the insertion would create (step 4)
+  u64 d_bytes;   // bytes the insertion would add (step 4)
+};
 struct orc_evict {
   u32 req, node_id, kind;  // kind 0 = leaf removal, 1 = merge (absorption)
   u32 n_live;              // live non-root nodes when this victim was chosen
@@ -356,6 +369,93 @@ struct Oracle {
     *hit_out = (u32)reuse;
     *flops_out = prefill_flops(reuse, model);
     *bypass_out = bypass ? 1u : 0u;
+  }
+
+  // ---- Lookup of request r (steps 1-4 of c.2, read-only) ----
+  void lookup(u32 r, orc_lookup* out) {
+    if (r < 1 || r > n_req) fail("request index out of range");
+    if (block) fail("lookup is defined for Marconi variants (block_size = 0)");
+    const std::vector<u32> S = seq(r);
+    const u64 n = S.size();
+    const u64 L_in = lin[r - 1];
+    if (L_in == 0) fail("input_len == 0 [c.3 #21]");
+    // Step 1: walk
+    std::vector<Node*> path;
+    Node* v = &root;
+    u64 pos = 0, m = 0;
+    Node* partial = nullptr;
+    Node* hit = nullptr;
+    u64 reuse = 0;
+    for (;;) {
+      if (pos == n) { m = n; break; }
+      auto it = v->children.find(S[pos]);
+      if (it == v->children.end()) { m = pos; break; }
+      Node* c = it->second;
+      u64 k = 0;
+      while (k < c->edge.size() && pos + k < n && c->edge[k] == S[pos + k]) k++;
+      path.push_back(c);
+      if (k == c->edge.size()) {
+        v = c;
+        pos += k;
+        if (c->has_ssm && depth_of(c) <= L_in) { hit = c; reuse = depth_of(c); }
+      } else {
+        m = pos + k;
+        partial = c;
+        break;
+      }
+    }
+    // Step 2: hit (n_ssm = 0: KVs sliced mid-edge)
+    if (model.n_ssm == 0) {
+      reuse = std::min(m, L_in);
+      hit = nullptr;
+      for (Node* x : path)
+        if (depth_of(x) - x->edge.size() < reuse) hit = x;
+    }
+    // Step 3: speculative insertion [c.3 #8, #9], chunked
+    const u64 m_in = std::min(m, L_in);
+    u64 q = 0;
+    if (m_in > 0) {
+      for (Node* x : path) {
+        u64 de = depth_of(x), ds = de - x->edge.size();
+        if (x != partial && de == m_in) {
+          if (!x->has_ssm) q = m_in;
+          break;
+        }
+        if (ds < m_in && m_in < de) { q = m_in; break; }
+      }
+    }
+    u64 p = q;
+    if (q && chunk) {
+      p = (q / chunk) * chunk;
+      if (p == 0 || p <= reuse) p = 0;
+    }
+    bool p_split = false;
+    if (p) {
+      for (Node* x : path) {
+        u64 de = depth_of(x), ds = de - x->edge.size();
+        if (x != partial && de == p) {
+          if (x->has_ssm) p = 0;  // the state already exists
+          break;
+        }
+        if (ds < p && p < de) { p_split = true; break; }
+      }
+    }
+    // Step 4: plan
+    u64 n_splits = (p_split ? 1 : 0) + ((partial && m < n && m != p) ? 1 : 0) + ((partial && m == n && n != p) ? 1 : 0);
+    const bool leaf = m < n;
+    const bool n_gain = !partial && m == n && !v->has_ssm && n != p;
+    u64 n_ckpt_new = (p ? 1 : 0) + ((n != p && (leaf || partial || n_gain)) ? 1 : 0);
+    const u64 ssmb = node_bytes(0, true, model), kvt = node_bytes(1, false, model);
+    Node* div = partial ? partial : v;
+    out->reuse = (u32)reuse;
+    out->m = (u32)m;
+    out->p = (u32)p;
+    out->hit_id = hit ? hit->id : 0;
+    out->div_id = div->id;
+    out->div_off = (u32)(m - (div == &root ? 0 : depth_of(div) - div->edge.size()));
+    out->path_len = (u32)path.size();
+    out->d_nodes = (u32)(n_splits + (leaf ? 1 : 0));
+    out->d_bytes = kvt * (n - m) + ssmb * n_ckpt_new;
   }
 
   // Node whose edge ends exactly at depth x along S (x must be a boundary).
@@ -752,6 +852,7 @@ int orc_log(void* h, orc_evict* out, u64 cap, u64* n_out) {
             std::copy(o->log.begin(), o->log.end(), out);
           })
 }
+int orc_lookup_req(void* h, u32 r, orc_lookup* out) { ORC_TRY(((Oracle*)h)->lookup(r, out)) }
 int orc_counters(void* h, u64* out4) {
   ORC_TRY(Oracle* o = (Oracle*)h; out4[0] = o->ctr_compared; out4[1] = o->ctr_visited;
           out4[2] = o->ctr_scanned; out4[3] = o->ctr_written)

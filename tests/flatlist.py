@@ -117,6 +117,58 @@ class FlatCache:
         return float(F(len(e.path), self.m) - F(pl, self.m)) / float(self.bytes(e))
 
     # ---- one request ----
+    def lookup(self, inp, out) -> dict:
+        """Steps 1-4 by brute force, read-only: m, reuse, the hit entry, the checkpoint p, the
+        entry where the match ends (mid-edge: the shortest extension; else the entry at m,
+        the root = id 0) with its matched edge length, |P| and the insertion plan."""
+        S = tuple(inp) + tuple(out)
+        n, L_in = len(S), len(inp)
+        m = max([_lcp(S, e.path) for e in self.E.values()] + [0])
+        hits = [e for e in self.E.values() if e.has_ssm and len(e.path) <= L_in and S[:len(e.path)] == e.path]
+        if self.m.n_ssm == 0:
+            reuse = min(m, L_in)
+            cont = [e for e in self.E.values() if len(e.path) > reuse - 1 and reuse > 0
+                    and e.path[:reuse] == S[:reuse] and self.parent_len(e) < reuse]
+            hit = cont[0] if cont else None
+        else:
+            hit = max(hits, key=lambda e: len(e.path)) if hits else None
+            reuse = len(hit.path) if hit else 0
+        full = [e for e in self.E.values() if len(e.path) <= m and S[:len(e.path)] == e.path]
+        m_mid = m > 0 and self.at(S, m) is None
+        partial = None
+        if m_mid:
+            ext = [e for e in self.E.values() if len(e.path) > m and e.path[:m] == S[:m]]
+            partial = min(ext, key=lambda e: len(e.path))
+        m_in = min(m, L_in)
+        q = 0
+        if m_in > 0:
+            b = self.at(S, m_in)
+            if b is None or not b.has_ssm:
+                q = m_in
+        p = q
+        if q and self.chunk:
+            p = (q // self.chunk) * self.chunk
+            if p == 0 or p <= reuse:
+                p = 0
+        p_split = False
+        if p:
+            b = self.at(S, p)
+            if b is None:
+                p_split = True
+            elif b.has_ssm:
+                p = 0
+        n_splits = int(p_split) + int(m_mid and m < n and m != p) + int(m_mid and m == n and n != p)
+        leaf = m < n
+        n_gain = (not m_mid and m == n and n != p and not self.at(S, n).has_ssm)
+        ck = (1 if p else 0) + (1 if n != p and (leaf or m_mid or n_gain) else 0)
+        div = partial if m_mid else self.at(S, m)
+        return {"reuse": reuse, "m": m, "p": p, "hit_id": hit.id if hit else 0,
+                "div_id": div.id if div is not None else 0,
+                "div_off": (m - self.parent_len(div)) if div is not None else 0,
+                "path_len": len(full) + (1 if partial else 0),
+                "d_nodes": n_splits + (1 if leaf else 0),
+                "d_bytes": KVT(self.m) * (n - m) + SSMB(self.m) * ck}
+
     def step(self, r: int, inp, out, chooser: Optional[Callable] = None):
         S = tuple(inp) + tuple(out)
         n, L_in = len(S), len(inp)
