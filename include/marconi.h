@@ -259,6 +259,32 @@ mc_status mc_replay(mc_ctx* ctx, const mc_replay_args* args, void* stream);
 mc_status mc_eviction_log(mc_ctx* ctx, const mc_replay_args* args, uint32_t variant, uint32_t alpha_idx,
                           uint32_t seg, mc_evict_rec* h_out, uint64_t cap, uint64_t* n_out, void* stream);
 
+/* Standalone batched lookup (SURVEY.md §8(a) a2-a3 as a query; PAPER:246, 300-301,
+ * 356-365, 371-373, 380): for each query, request `req` (1-based) of the trace is looked
+ * up against snapshot `snapshot` of `variant` (a frozen tree from mc_live_pass* or
+ * mc_set_snapshots) without changing it -- steps 1-4 of the replay: the walk, the hit,
+ * the speculative-insertion checkpoint and the insertion plan.  Marconi variants only
+ * (block_size = 0).  Queries are grouped by (variant, snapshot) on the host; one warp loads
+ * a snapshot image into its workspace slice and answers that group.  d_out[i] answers
+ * h_queries[i].  Workspace: mc_workspace_size(ctx, n_workers, 1, n_queries).  Async on
+ * `stream`; argument errors synchronous. */
+typedef struct {
+  uint32_t req, variant, snapshot, reserved;  /* reserved must be 0 */
+} mc_lookup_query;
+typedef struct {
+  uint32_t reuse;     /* skipped prefill tokens (the hit)                        */
+  uint32_t m;         /* matched length of the full sequence                                 */
+  uint32_t p;         /* speculative-insertion checkpoint position (0 = none)                */
+  uint32_t hit_id;    /* node whose state is reused (0 = none)                               */
+  uint32_t div_id;    /* node where the match ends: mid-edge node, else last full match (0 = root) */
+  uint32_t div_off;   /* m - d_start(div node)                                               */
+  uint32_t path_len;  /* fully matched nodes + the partially matched one                     */
+  uint32_t d_nodes;   /* nodes the insertion would create                                    */
+  uint64_t d_bytes;   /* bytes the insertion would add                                       */
+} mc_lookup_result;
+mc_status mc_lookup(mc_ctx* ctx, const mc_lookup_query* h_queries, uint32_t n_queries, void* d_workspace,
+                    uint64_t workspace_bytes, mc_lookup_result* d_out, void* stream);
+
 /* Synchronise `stream` and map the device status word to an mc_status. */
 mc_status mc_check(mc_ctx* ctx, void* stream);
 

@@ -220,6 +220,35 @@ __global__ void __launch_bounds__(32) live_kernel(KParams P) {
     P.live_cyc[(uint64_t)v * P.n_points + P.n_points - 1] = (unsigned long long)(clock64() - tw);
 }
 
+// Batched lookup (mc_lookup): warp w answers query groups w, w + n_workers, ...; a group
+// = the queries against one (variant, snapshot): its image is loaded into the warp's
+// workspace slice (private mode, dense list in the global tail) and every query walks it
+// read-only (lookup_request).  groups: {variant, snapshot, first, count} over perm.
+__global__ void __launch_bounds__(32) lookup_kernel(KParams P, const uint4* groups, uint32_t n_groups,
+                                                   const uint32_t* perm, const mc_lookup_query* q,
+                                                   mc_lookup_result* out) {
+  __shared__ __align__(16) DenseRec hdr[kSmemReserved];  // counters, constants, copy mbarrier (S = 0)
+  const uint32_t w = blockIdx.x;
+  if (*(volatile uint32_t*)P.status & ST_BADTRACE) return;
+  if (lane_id() == 0) {
+    mbar_init(reinterpret_cast<uint64_t*>(hdr + 12));
+    *reinterpret_cast<uint32_t*>(hdr + 13) = 0;
+  }
+  __syncwarp();
+  for (uint32_t gi = w; gi < n_groups; gi += P.n_workers) {
+    const uint4 g = groups[gi];
+    Chain C;
+    chain_init(C, P, w, P.var[g.x], 0.0, reinterpret_cast<char*>(hdr), 0, reinterpret_cast<ChainConst*>(hdr + 4),
+               reinterpret_cast<ChainCtr*>(hdr));
+    load_image(C, P, P.snap[g.x].img + P.snap[g.x].img_off[g.y]);
+    if (C.failed) continue;
+    for (uint32_t k = 0; k < g.w; k++) {
+      const uint32_t qi = perm[g.z + k];
+      lookup_request(C, P, q[qi].req, out + qi);
+    }
+  }
+}
+
 // Device-side trace check (mc_set_trace_async): the same rules as mc_set_trace's host
 // pass; a violation sets ST_BADTRACE and records the first bad request (1-based) in
 // status[1], so no request table ever travels back to the host.
@@ -1009,6 +1038,67 @@ mc_status mc_eviction_log(mc_ctx* c, const mc_replay_args* A, uint32_t v, uint32
     const uint64_t k = std::min<uint64_t>(std::min<uint64_t>(n, A->log_cap), cap);
     if (k) CU(cudaMemcpy(h_out, A->d_log + chain * A->log_cap, k * sizeof(mc_evict_rec), cudaMemcpyDeviceToHost));
   }
+  return MC_OK;
+}
+
+mc_status mc_lookup(mc_ctx* c, const mc_lookup_query* h_q, uint32_t n, void* d_ws, uint64_t ws_bytes,
+                    mc_lookup_result* d_out, void* stream) {
+  if (!c || (n && (!h_q || !d_ws || !d_out))) return fail(MC_EINVAL, "mc_lookup: null argument");
+  if (!c->tok) return fail(MC_ESTATE, "mc_lookup before mc_set_trace");
+  if (n == 0) return MC_OK;
+  const uint32_t nv = (uint32_t)c->hv.size();
+  std::vector<uint32_t> perm(n);
+  for (uint32_t i = 0; i < n; i++) {
+    const mc_lookup_query& q = h_q[i];
+    if (q.reserved) return fail(MC_EINVAL, "mc_lookup_query.reserved must be 0");
+    if (q.variant >= nv) return fail(MC_EINVAL, "query " + std::to_string(i) + ": variant out of range");
+    if (c->hv[q.variant].block_size) return fail(MC_EINVAL, "mc_lookup: vLLM+ variants (block_size > 0) have no lookup");
+    if (q.snapshot >= c->snaps[q.variant].count) return fail(MC_ESTATE, "query " + std::to_string(i) + ": no such snapshot");
+    if (q.req < 1 || q.req > c->n_req) return fail(MC_EINVAL, "query " + std::to_string(i) + ": request out of range");
+    perm[i] = i;
+  }
+  std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+    return h_q[a].variant != h_q[b].variant ? h_q[a].variant < h_q[b].variant : h_q[a].snapshot < h_q[b].snapshot;
+  });
+  std::vector<uint32_t> groups;  // {variant, snapshot, first, count} per group
+  for (uint32_t i = 0; i < n; i++) {
+    const mc_lookup_query& q = h_q[perm[i]];
+    const size_t G = groups.size();
+    if (G && groups[G - 4] == q.variant && groups[G - 3] == q.snapshot) groups[G - 1]++;
+    else { groups.push_back(q.variant); groups.push_back(q.snapshot); groups.push_back(i); groups.push_back(1); }
+  }
+  const uint32_t n_groups = (uint32_t)(groups.size() / 4);
+  // workspace: control header | worker slices | perm | groups | queries
+  const uint64_t tail = ((4ull * n + 15) & ~15ull) + 16ull * n_groups + sizeof(mc_lookup_query) * n;
+  const uint64_t per = ws_bytes_per_worker(c->ncap, c->hcap);
+  if (ws_bytes < kCtrl + per + tail) return fail(MC_ENOMEM, "workspace too small for mc_lookup");
+  const uint32_t workers = (uint32_t)std::min<uint64_t>((ws_bytes - kCtrl - tail) / per, n_groups);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)d_ws;
+  char* at = ws + kCtrl + (uint64_t)workers * per;
+  uint32_t* d_perm = (uint32_t*)at;
+  uint4* d_groups = (uint4*)(at + ((4ull * n + 15) & ~15ull));
+  mc_lookup_query* d_q = (mc_lookup_query*)((char*)d_groups + 16ull * n_groups);
+  CU(cudaMemcpyAsync(d_perm, perm.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_groups, groups.data(), 16ull * n_groups, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_q, h_q, sizeof(mc_lookup_query) * n, cudaMemcpyHostToDevice, st));
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.tok = c->tok;
+  P.n_tok = c->n_tok;
+  P.req = c->req;
+  P.n_req = c->n_req;
+  P.n_var = nv;
+  P.var = c->d_var;
+  P.snap = c->d_stores;
+  P.ncap = c->ncap;
+  P.hcap = c->hcap;
+  P.n_workers = workers;
+  P.ws = ws + kCtrl;
+  P.ws_stride = per;
+  P.status = c->d_status;
+  lookup_kernel<<<workers, 32, 0, st>>>(P, d_groups, n_groups, d_perm, d_q, d_out);
+  CU(cudaGetLastError());
   return MC_OK;
 }
 

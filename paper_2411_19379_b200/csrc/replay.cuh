@@ -2025,6 +2025,130 @@ __device__ ReqOut process_request_vllm(Chain& C, const KParams& P, uint32_t r, c
   return o;
 }
 
+// ---------------------------------------------------------------------------
+// Standalone lookup (mc_lookup): steps 1-4 of SURVEY.md §8(c) c.2 for request r against
+// the chain's current tree, read-only -- the walk (K2: child-index probe + warp compare,
+// PAPER:246, 300-301), the hit (all-or-nothing, or mid-edge KV reuse when n_ssm = 0), the
+// speculative-insertion checkpoint (chunk-aligned PAPER:371-373) and the
+// insertion plan.  Same rules as process_request steps 1-4.
+// ---------------------------------------------------------------------------
+__device__ void lookup_request(const Chain& C, const KParams& P, uint32_t r, mc_lookup_result* out) {
+  const uint32_t lane = lane_id();
+  const ReqHdr q = load_req(P, r);
+  const uint32_t off = q.off, L_in = q.lin, n = q.lin + q.lout;
+  uint32_t v = 0, v_ds = 0, pos = 0, npath = 0, m = 0, my_path = NIL, my_ds = 0, my_de = 0, my_fl = 0;
+  uint32_t partial = NIL, partial_ds = 0, hit = NIL, reuse = 0;
+  uint32_t lin_node = NIL, lin_bnd = NIL, v_flags = 0, lin_bnd_flags = 0;
+  uint32_t tk = __ldg(P.tok + off);
+  for (;;) {
+    if (pos == n) { m = n; break; }
+    const HEnt E = hash_find_warp(C, v, tk);
+    if (E.key == 0) { m = pos; break; }
+    const uint32_t c = E.key & SLOT14;
+    const uint32_t de = E.de & 0x7FFFFFFFu;
+    const uint32_t fl = E.de >> 31;
+    const uint32_t len = de - pos;
+    const uint32_t nt = (de < n) ? __ldg(P.tok + off + de) : 0u;
+    const uint32_t k = match_len(P.tok, (uint64_t)E.roff + pos, (uint64_t)off + pos, min(len, n - pos), P.n_tok);
+    if (lane == npath) { my_path = c; my_ds = pos; my_de = de; my_fl = fl; }
+    npath++;
+    if (pos < L_in && L_in < pos + len && L_in <= pos + k) lin_node = c;
+    if (k == len) {
+      v = c; v_ds = pos; v_flags = fl;
+      pos += len;
+      tk = nt;
+      if (de == L_in) { lin_bnd = c; lin_bnd_flags = fl; }
+      if ((fl & F_SSM) && de <= L_in) { hit = c; reuse = de; }
+    } else {
+      m = pos + k;
+      partial = c;
+      partial_ds = pos;
+      break;
+    }
+  }
+  // (the lanes hold the first 32 path nodes; deeper ones are reached by a parent walk)
+  if (C.K->m.n_ssm == 0) {  // pure Transformer: KVs sliced mid-edge
+    reuse = min(m, L_in);
+    hit = NIL;
+    uint32_t hi = NIL;
+    const bool mine = lane < min(npath, 32u) && my_ds < reuse;
+    const unsigned b = __ballot_sync(FULL, mine);
+    if (b) { hi = 31 - __clz(b); hit = __shfl_sync(FULL, my_path, hi); }
+    if (npath > 32) {  // deeper path nodes: walk the tree from the partial/last node upwards
+      uint32_t x = partial != NIL ? partial : v;
+      while (x != 0 && x != NIL) {
+        const NodeRec R = C.w.rec()[x];
+        if (R.ds < reuse) { hit = x; break; }
+        x = R.parent;
+      }
+    }
+  }
+  // step 3: speculative insertion of the input (R8, R9), chunk alignment (R11)
+  const uint32_t m_in = min(m, L_in);
+  uint32_t p = 0;
+  if (m_in > 0) {
+    if (m >= L_in) {
+      if (lin_bnd != NIL) { if (!(lin_bnd_flags & F_SSM)) p = m_in; }
+      else p = m_in;
+    } else if (partial != NIL) {
+      p = m_in;
+    } else if (!(v_flags & F_SSM)) {
+      p = m_in;
+    }
+  }
+  bool p_split = (p != 0) && ((m >= L_in) ? (lin_bnd == NIL) : (partial != NIL));
+  if (C.K->chunk && p) {
+    uint32_t pa = (p / C.K->chunk) * C.K->chunk;
+    if (pa == 0 || pa <= reuse) pa = 0;
+    p_split = false;
+    if (pa) {
+      // the node at or containing pa on the path: lanes < 32, deeper ones by a parent walk
+      const bool mine = lane < min(npath, 32u);
+      const unsigned bnd = __ballot_sync(FULL, mine && my_de == pa && my_path != partial);
+      const unsigned ins = __ballot_sync(FULL, mine && my_ds < pa && pa < my_de);
+      if (bnd) {
+        if (__shfl_sync(FULL, my_fl, __ffs(bnd) - 1) & F_SSM) pa = 0;
+      } else if (ins) {
+        p_split = true;
+      } else {
+        uint32_t kind = 0;
+        uint32_t x = partial != NIL ? partial : v;
+        while (x != 0 && x != NIL) {
+          const NodeRec R = C.w.rec()[x];
+          if (x != partial && R.de == pa) { kind = ((R.nf >> 24) & F_SSM) ? 3 : 1; break; }
+          if (R.ds < pa && pa < R.de) { kind = 2; break; }
+          x = R.parent;
+        }
+        if (kind == 2) p_split = true;
+        else if (kind != 1) pa = 0;
+      }
+    }
+    p = pa;
+  }
+  // step 4: plan
+  const bool leaf = m < n;
+  const bool split_m = partial != NIL && m < n && m != p;
+  const bool split_n = partial != NIL && m == n && n != p;
+  const bool n_gain = partial == NIL && m == n && n != p && !(v_flags & F_SSM);
+  uint32_t n_ck = p ? 1u : 0u;
+  if (n != p && (leaf || split_n || n_gain)) n_ck++;
+  if (lane == 0) {
+    mc_lookup_result o;
+    o.reuse = reuse;
+    o.m = m;
+    o.p = p;
+    o.hit_id = hit == NIL ? 0u : C.w.rec()[hit].id;
+    const uint32_t dv = partial != NIL ? partial : v;
+    o.div_id = dv == 0 ? 0u : C.w.rec()[dv].id;
+    o.div_off = m - (partial != NIL ? partial_ds : v_ds);
+    o.path_len = npath;
+    o.d_nodes = (p_split ? 1u : 0u) + (split_m ? 1u : 0u) + (split_n ? 1u : 0u) + (leaf ? 1u : 0u);
+    o.d_bytes = C.K->m.kvt * (uint64_t)(n - m) + C.K->m.ssmb * n_ck;
+    *out = o;
+  }
+  __syncwarp();
+}
+
 // kc / kx: shared memory for the chain's constants and counters (written by lane 0 here).
 __device__ __forceinline__ void chain_init(Chain& C, const KParams& P, uint32_t worker, const DevVariant& V,
                                            double alpha, char* smem_warp, uint32_t S, ChainConst* kc, ChainCtr* kx) {

@@ -23,12 +23,16 @@ SNAP_DTYPE = np.dtype([("id", "<u4"), ("parent_id", "<u4"), ("ref_off", "<u8"), 
 SEGMENT_DTYPE = np.dtype([("first_req", "<u4"), ("n_req", "<u4"), ("snapshot", "<u4"), ("reserved", "<u4")])
 EVICT_DTYPE = np.dtype([("req", "<u4"), ("node_id", "<u4"), ("kind", "<u4"), ("n_live", "<u4"),
                         ("utility", "<f8")], align=True)
+QUERY_DTYPE = np.dtype([("req", "<u4"), ("variant", "<u4"), ("snapshot", "<u4"), ("reserved", "<u4")])
+LOOKUP_DTYPE = np.dtype([("reuse", "<u4"), ("m", "<u4"), ("p", "<u4"), ("hit_id", "<u4"), ("div_id", "<u4"),
+                         ("div_off", "<u4"), ("path_len", "<u4"), ("d_nodes", "<u4"), ("d_bytes", "<u8")])
 assert REQUEST_DTYPE.itemsize == 16 and SNAP_DTYPE.itemsize == 32 and EVICT_DTYPE.itemsize == 24
+assert QUERY_DTYPE.itemsize == 16 and LOOKUP_DTYPE.itemsize == 40
 
 EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at", "mc_live_pass_bootstrap",
             "mc_snapshot_count", "mc_live_window_cycles",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
-            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log")
+            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log", "mc_lookup")
 
 MC_STATUS = {0: "MC_OK", -1: "MC_EINVAL", -2: "MC_ENOMEM", -3: "MC_ECUDA", -4: "MC_EOVERFLOW",
              -5: "MC_ESTATE", -6: "MC_EDEVICE"}
@@ -87,6 +91,7 @@ def lib():
             "mc_workspace_workers": [P, U64, U32, U32, P],
             "mc_replay": [P, P, P],
             "mc_check": [P, P],
+            "mc_lookup": [P, P, U32, P, U64, P, P],
             "mc_eviction_log": [P, P, U32, U32, U32, P, U64, P, P],
             "mc_node_cost": [P, U32, P, P, P, P, P, P, P],
             "mc_score_argmin": [U32, P, P, P, P, P, P, P, P, P],
@@ -348,6 +353,31 @@ class Context:
         self._last_args = (alph, ch, ws, args)
         check(lib().mc_replay(self.h, C.byref(args), _stream_ptr(stream)))
         return out
+
+    def lookup(self, req, variant=0, snapshot=0, workspace=None, stream=None):
+        """Batched read-only lookup (mc_lookup) of requests `req` (1-based, array) against
+        snapshot `snapshot` of `variant` (scalars or arrays).  Returns a device uint8 tensor
+        viewable as LOOKUP_DTYPE records (see lookup_records)."""
+        torch = self.torch
+        req = np.atleast_1d(np.asarray(req, np.uint32))
+        q = np.zeros(req.shape[0], QUERY_DTYPE)
+        q["req"] = req
+        q["variant"] = variant
+        q["snapshot"] = snapshot
+        n = q.shape[0]
+        n_groups = len(set(zip(q["variant"].tolist(), q["snapshot"].tolist())))
+        if workspace is None:
+            workspace = self.alloc_workspace(min(n_groups, 4 * 148), 1, 0)
+            workspace = torch.cat([workspace, torch.zeros(64 * n + 4096, dtype=torch.uint8, device=self.device)])
+        out = torch.zeros(n * LOOKUP_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+        check(lib().mc_lookup(self.h, _np_ptr(q), n, _tptr(workspace), workspace.numel(), _tptr(out),
+                              _stream_ptr(stream)))
+        self._last_lookup = (q, workspace)
+        return out
+
+    @staticmethod
+    def lookup_records(out) -> np.ndarray:
+        return out.cpu().numpy().view(LOOKUP_DTYPE).copy()
 
     def alloc_outputs(self, n_alpha: int, log_cap: int = 0, counters: bool = False, chain_cycles: bool = False):
         torch = self.torch
