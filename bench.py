@@ -428,6 +428,9 @@ def main():
     if not args.no_e2e:
         e2e = e2e_measure(gs, ws, args, outs, shared)
 
+    # the paper's metrics at α* (this rank's chains), from the device sums
+    met = gs[0].metrics(outs[0])
+    hit_rate_at_star = [round(met.get((v, a_star[0][v]), (0.0, 0))[0], 6) for v in range(len(w.variants))]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_seconds)
@@ -442,6 +445,7 @@ def main():
                                                  f"{'gloo' if shared else 'NCCL'} all-gather of per-(problem, alpha) "
                                                  f"hit sums per step",
                            alpha_star=[a[0] for a in a_star],
+                           token_hit_rate_at_alpha_star=hit_rate_at_star if world == 1 else None,
                            schedule="persistent queue, chains longest-first: the first replay by the live pass's "
                                     "per-segment cycles, later ones by the previous replay's per-chain cycles",
                            first_replay_ms=first_ms,

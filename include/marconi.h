@@ -259,6 +259,14 @@ mc_status mc_replay(mc_ctx* ctx, const mc_replay_args* args, void* stream);
 mc_status mc_eviction_log(mc_ctx* ctx, const mc_replay_args* args, uint32_t variant, uint32_t alpha_idx,
                           uint32_t seg, mc_evict_rec* h_out, uint64_t cap, uint64_t* n_out, void* stream);
 
+/* Per-chain sums of a replay's outputs (token hit rate = skipped prefill
+ * tokens / input tokens; FLOPs saved): for each chain id d_chains[i] (device, as passed to
+ * mc_replay), d_out[4i .. 4i+3] = {Σ hit, Σ input_len, Σ FLOPs saved low 64 bits, high 64
+ * bits} over the chain's segment window, read from the replay's d_hit / d_flops
+ * ([n_variants][n_alpha][n_reqs]).  One warp per chain, async on `stream`. */
+mc_status mc_chain_sums(mc_ctx* ctx, uint32_t n_alpha, const uint32_t* d_hit, const uint64_t* d_flops,
+                        const uint32_t* d_chains, uint32_t n_chains, uint64_t* d_out, void* stream);
+
 /* Standalone batched lookup (SURVEY.md §8(a) a2-a3 as a query; PAPER:246, 300-301,
  * 356-365, 371-373, 380): for each query, request `req` (1-based) of the trace is looked
  * up against snapshot `snapshot` of `variant` (a frozen tree from mc_live_pass* or

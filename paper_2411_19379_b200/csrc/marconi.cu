@@ -249,6 +249,43 @@ __global__ void __launch_bounds__(32) lookup_kernel(KParams P, const uint4* grou
   }
 }
 
+// Per-chain sums of a replay's outputs (mc_chain_sums; PAPER:537-538 metrics): one warp
+// per chain (variant, α, segment) reduces its window's hits, input tokens and FLOPs saved;
+// FLOPs in 128-bit (a window's sum can pass 2^64).  out[i] = {Σhit, ΣL_in, Σflops lo, hi}.
+__global__ void chain_sums_kernel(const mc_request* req, const mc_segment* segs, uint32_t n_segs, uint32_t n_alpha,
+                                  uint32_t n_req, const uint32_t* chains, uint32_t n_chains, const uint32_t* hit,
+                                  const unsigned long long* flops, unsigned long long* out) {
+  const uint32_t lane = lane_id();
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n_chains) return;
+  const uint32_t c = chains[i];
+  const uint32_t s = c % n_segs, a = (c / n_segs) % n_alpha, v = c / (n_segs * n_alpha);
+  const mc_segment seg = segs[s];
+  const uint64_t base = ((uint64_t)v * n_alpha + a) * n_req;
+  unsigned long long sh = 0, sl = 0;
+  unsigned __int128 sf = 0;
+  for (uint32_t k = lane; k < seg.n_req; k += 32) {
+    const uint32_t r = seg.first_req + k;
+    sh += hit[base + r - 1];
+    sl += req[r - 1].input_len;
+    sf += flops[base + r - 1];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sh += __shfl_xor_sync(FULL, sh, o);
+    sl += __shfl_xor_sync(FULL, sl, o);
+    const unsigned long long lo = __shfl_xor_sync(FULL, (unsigned long long)sf, o);
+    const unsigned long long hi = __shfl_xor_sync(FULL, (unsigned long long)(sf >> 64), o);
+    sf += ((unsigned __int128)hi << 64) | lo;
+  }
+  if (lane == 0) {
+    out[4ull * i + 0] = sh;
+    out[4ull * i + 1] = sl;
+    out[4ull * i + 2] = (unsigned long long)sf;
+    out[4ull * i + 3] = (unsigned long long)(sf >> 64);
+  }
+}
+
 // Device-side trace check (mc_set_trace_async): the same rules as mc_set_trace's host
 // pass; a violation sets ST_BADTRACE and records the first bad request (1-based) in
 // status[1], so no request table ever travels back to the host.
@@ -1038,6 +1075,20 @@ mc_status mc_eviction_log(mc_ctx* c, const mc_replay_args* A, uint32_t v, uint32
     const uint64_t k = std::min<uint64_t>(std::min<uint64_t>(n, A->log_cap), cap);
     if (k) CU(cudaMemcpy(h_out, A->d_log + chain * A->log_cap, k * sizeof(mc_evict_rec), cudaMemcpyDeviceToHost));
   }
+  return MC_OK;
+}
+
+mc_status mc_chain_sums(mc_ctx* c, uint32_t n_alpha, const uint32_t* d_hit, const uint64_t* d_flops,
+                        const uint32_t* d_chains, uint32_t n_chains, uint64_t* d_out, void* stream) {
+  if (!c || !d_hit || !d_flops || (n_chains && (!d_chains || !d_out)) || n_alpha == 0)
+    return fail(MC_EINVAL, "mc_chain_sums: bad argument");
+  if (!c->tok || c->segs.empty()) return fail(MC_ESTATE, "mc_chain_sums before mc_set_trace/mc_set_segments");
+  if (n_chains == 0) return MC_OK;
+  const uint32_t ns = (uint32_t)c->segs.size();
+  chain_sums_kernel<<<(n_chains + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      c->req, c->d_segs, ns, n_alpha, c->n_req, d_chains, n_chains, d_hit, (const unsigned long long*)d_flops,
+      (unsigned long long*)d_out);
+  CU(cudaGetLastError());
   return MC_OK;
 }
 

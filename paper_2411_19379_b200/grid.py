@@ -157,6 +157,18 @@ class AlphaGrid:
     def run(self, out=None, **kw):
         return self.ctx.replay(self.alphas, chains=self.chains, workspace=self.workspace, out=out, **kw)
 
+    def metrics(self, out):
+        """This rank's per-(variant, α) token hit rate (Σ skipped prefill tokens / Σ input
+        tokens) and exact Σ FLOPs saved, from the device per-chain
+        sums (mc_chain_sums).  Returns {(v, α): (hit_rate, flops_saved)}."""
+        na, ns = len(self.alphas), len(self.segs)
+        acc = {}
+        for c, (sh, sl, sf) in zip(self.chains.tolist(), self.ctx.chain_sums(out, na, self.chains)):
+            key = (c // (na * ns), self.alphas[(c // ns) % na])
+            h, l, f = acc.get(key, (0, 0, 0))
+            acc[key] = (h + sh, l + sl, f + sf)
+        return {k: (h / l if l else 0.0, f) for k, (h, l, f) in acc.items()}
+
     def reorder_by_cycles(self, cycles) -> None:
         """Cost feedback: order this rank's chains longest-first by the per-chain cycles a
         previous replay of the same chains measured (outputs["cycles"]); the persistent

@@ -32,7 +32,7 @@ assert QUERY_DTYPE.itemsize == 16 and LOOKUP_DTYPE.itemsize == 40
 EXPORTED = ("mc_create", "mc_destroy", "mc_set_trace", "mc_set_trace_async", "mc_set_snapshots", "mc_live_pass", "mc_live_pass_at", "mc_live_pass_bootstrap",
             "mc_snapshot_count", "mc_live_window_cycles",
             "mc_get_snapshot", "mc_set_segments", "mc_workspace_size", "mc_workspace_workers", "mc_replay",
-            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log", "mc_lookup")
+            "mc_check", "mc_last_error", "mc_node_cost", "mc_score_argmin", "mc_eviction_log", "mc_lookup", "mc_chain_sums")
 
 MC_STATUS = {0: "MC_OK", -1: "MC_EINVAL", -2: "MC_ENOMEM", -3: "MC_ECUDA", -4: "MC_EOVERFLOW",
              -5: "MC_ESTATE", -6: "MC_EDEVICE"}
@@ -92,6 +92,7 @@ def lib():
             "mc_replay": [P, P, P],
             "mc_check": [P, P],
             "mc_lookup": [P, P, U32, P, U64, P, P],
+            "mc_chain_sums": [P, U32, P, P, P, U32, P, P],
             "mc_eviction_log": [P, P, U32, U32, U32, P, U64, P, P],
             "mc_node_cost": [P, U32, P, P, P, P, P, P, P],
             "mc_score_argmin": [U32, P, P, P, P, P, P, P, P, P],
@@ -374,6 +375,17 @@ class Context:
                               _stream_ptr(stream)))
         self._last_lookup = (q, workspace)
         return out
+
+    def chain_sums(self, out, n_alpha: int, chains, stream=None):
+        """Per chain (device replay outputs, mc_chain_sums): list of (Σ hit, Σ input tokens,
+        Σ FLOPs saved as an exact Python int)."""
+        torch = self.torch
+        ch = torch.from_numpy(np.ascontiguousarray(chains, np.uint32).view(np.int32)).to(self.device)
+        res = torch.zeros((ch.numel(), 4), dtype=torch.int64, device=self.device)
+        check(lib().mc_chain_sums(self.h, n_alpha, _tptr(out["hit"]), _tptr(out["flops"]), _tptr(ch), ch.numel(),
+                                  _tptr(res), _stream_ptr(stream)))
+        r = res.cpu().numpy().view(np.uint64)
+        return [(int(a), int(b), int(c) | (int(d) << 64)) for a, b, c, d in r]
 
     @staticmethod
     def lookup_records(out) -> np.ndarray:

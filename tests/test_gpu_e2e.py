@@ -121,3 +121,23 @@ def test_cost_feedback_order_changes_no_result():
     g.ctx.check()
     for k in ("hit", "flops", "bypass", "hit_sum"):
         assert torch.equal(out[k], out2[k]), k
+
+
+def test_chain_sums_match_outputs():
+    """mc_chain_sums: per chain Σ hit, Σ input tokens and Σ FLOPs saved (exact, 128-bit)
+    equal the sums of the replay's per-request outputs over the chain's window."""
+    w = tg.workload(3, R=5000)
+    g = AlphaGrid(w.trace, w.variants, w.alphas, w.n_segments).setup()
+    out = g.run()
+    g.ctx.check()
+    sums = g.ctx.chain_sums(out, len(w.alphas), g.chains)
+    hit = out["hit"].cpu().numpy()
+    fl = out["flops"].cpu().numpy().astype(np.uint64)
+    na, ns = len(w.alphas), len(g.segs)
+    for c, (sh, sl, sf) in zip(g.chains.tolist(), sums):
+        v, a, s = c // (na * ns), (c // ns) % na, c % ns
+        f, n, _ = g.segs[s]
+        sl_ref = int(w.trace.lin[f - 1:f - 1 + n].astype(np.int64).sum())
+        assert sh == int(hit[v, a, f - 1:f - 1 + n].astype(np.int64).sum())
+        assert sl == sl_ref
+        assert sf == sum(int(x) for x in fl[v, a, f - 1:f - 1 + n])
