@@ -441,15 +441,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": T_ms / args.steps,
             "ms_per_step_median": float(np.median(step_ms)), "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": dict(config, parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one "
-                                                 f"{'gloo' if shared else 'NCCL'} all-gather of per-(problem, alpha) "
-                                                 f"hit sums per step",
-                           alpha_star=[a[0] for a in a_star],
-                           token_hit_rate_at_alpha_star=hit_rate_at_star if world == 1 else None,
-                           schedule="persistent queue, chains longest-first: the first replay by the live pass's "
-                                    "per-segment cycles, later ones by the previous replay's per-chain cycles",
-                           first_replay_ms=first_ms,
-                           setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
+            # config: the workload only, identical to the reference arm's; run-specific facts in "run"
+            "config": config,
+            "run": dict(parallelism=f"chains of every problem LPT-sharded over {world} GPU(s); one "
+                                    f"{'gloo' if shared else 'NCCL'} all-gather of per-(problem, alpha) "
+                                    f"hit sums per step",
+                        alpha_star=[a[0] for a in a_star],
+                        token_hit_rate_at_alpha_star=hit_rate_at_star if world == 1 else None,
+                        schedule="persistent queue, chains longest-first: the first replay by the live pass's "
+                                 "per-segment cycles, later ones by the previous replay's per-chain cycles",
+                        first_replay_ms=first_ms,
+                        setup_s={"trace_gen": round(t_gen, 2), "upload_live_pass_shard": round(t_setup, 2)}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "replay_kernel<%d>" % (args.policy == "vllm"), "alg_bytes_per_launch": alg_bytes,
