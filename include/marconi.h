@@ -263,7 +263,8 @@ mc_status mc_eviction_log(mc_ctx* ctx, const mc_replay_args* args, uint32_t vari
  * tokens / input tokens; FLOPs saved): for each chain id d_chains[i] (device, as passed to
  * mc_replay), d_out[4i .. 4i+3] = {Σ hit, Σ input_len, Σ FLOPs saved low 64 bits, high 64
  * bits} over the chain's segment window, read from the replay's d_hit / d_flops
- * ([n_variants][n_alpha][n_reqs]).  One warp per chain, async on `stream`. */
+ * ([n_variants][n_alpha][n_reqs]).  One warp per chain, async on `stream`; a chain id
+ * outside [0, n_variants * n_alpha * n_segments) is skipped and flagged for mc_check. */
 mc_status mc_chain_sums(mc_ctx* ctx, uint32_t n_alpha, const uint32_t* d_hit, const uint64_t* d_flops,
                         const uint32_t* d_chains, uint32_t n_chains, uint64_t* d_out, void* stream);
 

@@ -253,12 +253,17 @@ __global__ void __launch_bounds__(32) lookup_kernel(KParams P, const uint4* grou
 // per chain (variant, α, segment) reduces its window's hits, input tokens and FLOPs saved;
 // FLOPs in 128-bit (a window's sum can pass 2^64).  out[i] = {Σhit, ΣL_in, Σflops lo, hi}.
 __global__ void chain_sums_kernel(const mc_request* req, const mc_segment* segs, uint32_t n_segs, uint32_t n_alpha,
-                                  uint32_t n_req, const uint32_t* chains, uint32_t n_chains, const uint32_t* hit,
-                                  const unsigned long long* flops, unsigned long long* out) {
+                                  uint32_t n_var, uint32_t n_req, const uint32_t* chains, uint32_t n_chains,
+                                  const uint32_t* hit, const unsigned long long* flops, unsigned long long* out,
+                                  uint32_t* status) {
   const uint32_t lane = lane_id();
   const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= n_chains) return;
   const uint32_t c = chains[i];
+  if ((uint64_t)c >= (uint64_t)n_var * n_alpha * n_segs) {  // not a chain id of this context
+    if (lane == 0) atomicOr(status, ST_INVARIANT);
+    return;
+  }
   const uint32_t s = c % n_segs, a = (c / n_segs) % n_alpha, v = c / (n_segs * n_alpha);
   const mc_segment seg = segs[s];
   const uint64_t base = ((uint64_t)v * n_alpha + a) * n_req;
@@ -1086,8 +1091,8 @@ mc_status mc_chain_sums(mc_ctx* c, uint32_t n_alpha, const uint32_t* d_hit, cons
   if (n_chains == 0) return MC_OK;
   const uint32_t ns = (uint32_t)c->segs.size();
   chain_sums_kernel<<<(n_chains + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      c->req, c->d_segs, ns, n_alpha, c->n_req, d_chains, n_chains, d_hit, (const unsigned long long*)d_flops,
-      (unsigned long long*)d_out);
+      c->req, c->d_segs, ns, n_alpha, (uint32_t)c->hv.size(), c->n_req, d_chains, n_chains, d_hit,
+      (const unsigned long long*)d_flops, (unsigned long long*)d_out, c->d_status);
   CU(cudaGetLastError());
   return MC_OK;
 }
