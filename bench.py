@@ -310,13 +310,17 @@ def main():
     # N problems (weak scaling): the chains of EVERY problem are LPT-sharded across all
     # ranks, so each rank replays ~one problem's worth of chains and the per-(problem, α)
     # hit sums must be all-gathered before any rank can pick α*.
+    # NVTX ranges mark the phases (setup, replay, all-gather + α*, e2e) for an nsys timeline
+    nvtx = torch.cuda.nvtx
     t_setup = time.perf_counter()
+    nvtx.range_push("setup: trace H2D + live pass + snapshot images + shard")
     gs = []
     for k, wk in enumerate(ws):
         g = AlphaGrid(wk.trace, wk.variants, wk.alphas, wk.n_segments, rank=rank, world=world, device=dev)
         g.setup()
         gs.append(g)
     torch.cuda.synchronize()
+    nvtx.range_pop()
     t_setup = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream()
     streams = [torch.cuda.Stream() for _ in gs] if len(gs) > 1 else [stream]
@@ -326,6 +330,7 @@ def main():
     all_reqs = sum(sum(n for _, n, _ in g.segs) * len(w.alphas) * len(w.variants) for g in gs)
 
     def launch():
+        nvtx.range_push("replay: alpha-grid chains")
         ev = torch.cuda.Event()
         ev.record(stream)
         ends = []
@@ -339,11 +344,15 @@ def main():
                 ends.append(e)
         for e in ends:
             stream.wait_event(e)
+        nvtx.range_pop()
 
     def select():
+        nvtx.range_push("select: all-gather of hit sums + alpha*")
         hs = torch.stack([o["hit_sum"] for o in outs])          # [problem, variant, alpha]
         tot = gather_hit_sums(hs, world)                        # one all-gather over NCCL
-        return [g.select(o, gathered=tot[k]) for k, (g, o) in enumerate(zip(gs, outs))]
+        res = [g.select(o, gathered=tot[k]) for k, (g, o) in enumerate(zip(gs, outs))]
+        nvtx.range_pop()
+        return res
 
     if args.traffic_probe:  # child of traffic_probe(): one warm launch, then the launch ncu measures
         for _ in range(2):
@@ -426,7 +435,9 @@ def main():
     # e2e through the public API with host buffers (this rank's shards of every problem)
     e2e = None
     if not args.no_e2e:
+        nvtx.range_push("e2e: host-buffer pipeline")
         e2e = e2e_measure(gs, ws, args, outs, shared)
+        nvtx.range_pop()
 
     # the paper's metrics at α* (this rank's chains), from the device sums
     met = gs[0].metrics(outs[0])
