@@ -26,3 +26,16 @@ def test_ttft_proxy_closed_forms():
 
 def test_default_throughput_is_labelled_fraction_of_measured_peak():
     assert 100.0 < RP.default_prefill_tflops() < 2250.0
+
+
+def test_markdown_tables_cover_every_section():
+    row = {"case": "x", "hit_vllm+": 0.1, "hit_sglang+": 0.5, "hit_marconi": 0.6, "alpha_star": 0.25,
+           "marconi_vs_vllm+": 6.0, "marconi_vs_sglang+": 1.2,
+           "ttft_p95_rel_no_cache": {"vllm+": 0.9, "sglang+": 0.5, "marconi": 0.4},
+           "ttft_proxy_ms": {}}
+    rep = {"prefill_tflops_assumed": 500.0, "ttft_note": "proxy", "data": "synthetic"}
+    for sec in ("main", "state_dim", "arrival", "cache_size", "ratio"):
+        rep[sec] = [dict(row, case=sec)]
+    md = RP.to_markdown(rep)
+    for sec in ("main", "state_dim", "arrival", "cache_size", "ratio"):
+        assert f"## {sec}" in md and f"| {sec} | 10.0 % | 50.0 % | 60.0 % (0.25) | 6.00 | 1.20 |" in md
