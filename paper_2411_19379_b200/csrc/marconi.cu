@@ -4,9 +4,16 @@
 // a dense contraction):
 //   replay_kernel     K5: persistent; each warp pops chains (variant, α, segment)
 //                     from a device queue, loads the segment snapshot and
-//                     replays the window (K1-K4 inlined, see replay.cuh).
+//                     replays the window (K1-K4 inlined, see replay.cuh); a lean
+//                     Marconi instantiation (no log / chunk / n_ssm = 0 paths), a
+//                     general one, and the vLLM+ one.
 //   live_kernel       the α = 0 live LRU pass per variant, dumping snapshot k
-//                     after every `window` requests (segment mode, R19).
+//                     after every `window` requests (segment mode, R19) or at the
+//                     bootstrap points, with per-window cycle counts.
+//   image_kernel      loadable snapshot images.
+//   lookup_kernel     mc_lookup: read-only lookups against frozen snapshots.
+//   chain_sums_kernel mc_chain_sums: per-chain Σ hit / Σ L_in / 128-bit Σ FLOPs.
+//   trace_check_kernel  mc_set_trace_async: the trace rules on the device.
 //   snap_link_kernel  resolves parent ids of uploaded canonical snapshots.
 //   node_cost_kernel  K1 batched (unit parity).
 //   score_argmin_kernel  K3 segmented, one warp per table (unit parity).

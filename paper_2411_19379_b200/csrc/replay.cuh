@@ -3,22 +3,26 @@
 // One WARP owns one chain (variant, α, segment): a private flattened radix
 // tree replayed request by request.
 //
-// Data layout per chain (DESIGN.md "Layout"):
-//   shared memory  dense live-node list: t_last|pin|multi (u32) and RN32(FLOP efficiency)
-//                  (f64) for positions < S -- the data every eviction scans;
-//   global (L2)    32-byte AoS node records {parent, first token, d_start, d_end |
-//                  id, child xor, nchild|flags, dense position}, u32 pool offsets,
-//                  a 4-byte-entry open-addressing child index keyed by (parent,
-//                  first token) whose entries carry a generation tag (no table
-//                  clear between chains), the dense tail (positions >= S).
+// Data layout per chain (DESIGN.md §6):
+//   shared memory  dense list by node slot: t_last|pin|multi (u32) and RN32(FLOP
+//                  efficiency) (f32) for slots < S -- the data every eviction scans --
+//                  then the counters, constants and the snapshot-copy mbarrier;
+//   global (L2)    32-byte node records {parent, own child-index position, d_start,
+//                  d_end, pool offset, child xor, nchild|flags, id}; a 16-byte-entry
+//                  open-addressing child index keyed by (parent, first token) whose
+//                  entries carry the child's slot, depth, state flag and pool offset
+//                  plus a generation tag (no table clear between chains); the dense
+//                  tail (slots >= S).  The exact fp64 eff is recomputed from a record
+//                  when a cold path needs it.
 // Warp-cooperative stages:
-//   K2 walk      -- child lookup = 32-wide linear-probe window (one 128 B line of
-//                   entries + the candidates' records in parallel); edge compare =
-//                   128 tokens per step with __ballot_sync/__ffs (PAPER:246,
-//                   PAPER:300-301; speculative insertion PAPER:365 fused in);
+//   K2 walk      -- child lookup = one 128 B line of the index per probe step; edge
+//                   compare = 8 x 32 tokens per round trip with __ballot_sync/__ffs,
+//                   long compares prefetched into L2 by cp.async.bulk.prefetch
+//                   (speculative insertion PAPER:365 fused in);
 //   K3 scan      -- normalisation bounds + filter-and-verify argmin of Eq. 2
 //                   (PAPER:414-419), warp-shuffle reductions;
-//   snapshot load / dump -- 32 nodes per step.
+//   snapshot image load -- dense list by one cp.async.bulk (TMA) into shared memory;
+//   lookup       -- mc_lookup's read-only steps 1-4 (lookup_request).
 // Scalar tree mutations (K4: split, leaf, gain, leaf removal, absorption --
 // PAPER:362-365) run on lane 0; the chain scalars are then
 // broadcast.  K1 (Eq. 1 cost model, Appendix A) is inlined wherever a node's
