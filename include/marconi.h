@@ -219,8 +219,9 @@ mc_status mc_workspace_workers(const mc_ctx* ctx, uint64_t bytes, uint32_t n_alp
 typedef struct {
   const double* h_alphas;   /* [n_alpha], each >= 0 and not NaN            */
   uint32_t n_alpha;
-  const uint32_t* h_chains; /* chain ids to run on this call (this rank's shard);     */
-  uint32_t n_chains;        /* NULL = all chains                                      */
+  const uint32_t* h_chains; /* chain ids to run on this call (this rank's shard), in  */
+  uint32_t n_chains;        /* the order warps take them (longest first packs best);
+                               NULL = all chains in id order                          */
   void* d_workspace;
   uint64_t workspace_bytes;
   uint32_t* d_hit;          /* [n_variants][n_alpha][n_reqs]  hit tokens per request   */
@@ -233,7 +234,7 @@ typedef struct {
   mc_evict_rec* d_log;      /* [n_chains_total][log_cap] nullable: eviction log        */
   uint32_t log_cap;
   uint32_t* d_log_n;        /* [n_chains_total] records produced (may exceed log_cap)  */
-  uint32_t* d_chain_ns;     /* [n_chains_total] nullable: per-chain clock64 cycles      */
+  uint32_t* d_chain_ns;     /* [n_chains_total] nullable: per-chain SM cycles / 1024    */
   uint32_t n_workers;       /* 0 = default (derived from the workspace size)          */
   uint32_t smem_nodes;      /* dense live-list positions per chain held in shared
                                memory (0 = auto: fill the SM at the target occupancy) */
