@@ -8,4 +8,4 @@ run() { f=$1; shift; echo "== $f $*"; env "$@" MARCONI_LIB=$PWD/build/variants/$
 for i in 1 2 3; do
 for f in build/variants/*.so; do case $f in *t3*) continue;; esac; run $(basename $f) A=1; done
 done
-for f in build/variants/*t3*.so; do [ -e "$f" ] && TAILN=22 run $(basename $f) PHASES3A=1 CHAINS=1; done
+for f in build/variants/*t3*.so; do [ -e "$f" ] && TAILN=24 run $(basename $f) PHASES3=1 PHASES3A=1 CHAINS=1; done

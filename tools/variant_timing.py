@@ -39,11 +39,17 @@ if os.environ.get("PHASES"):
 if os.environ.get("PHASES3"):
     c = ctr.astype(np.uint64)
     nreq = len(g.chains) * w.window
-    sel, p2, rem = (c[:, k].astype(np.float64).sum() / nreq / 1e3 for k in range(3))
+    m40 = np.uint64((1 << 40) - 1)
+    sel = c[:, 0].astype(np.float64).sum() / nreq / 1e3
+    p2 = (c[:, 1] & m40).astype(np.float64).sum() / nreq / 1e3
+    fp = float((c[:, 1] >> np.uint64(40)).sum()) / nreq
+    rem = (c[:, 2] & m40).astype(np.float64).sum() / nreq / 1e3
+    sl = float((c[:, 2] >> np.uint64(40)).sum()) / nreq
     p1 = float((c[:, 3] >> np.uint64(32)).sum()) / nreq
-    fb = float((c[:, 3] & np.uint64(0xFFFFFFFF)).sum()) / nreq
-    print("per request k-cycles: select %.1f (pass2 %.1f) removal %.1f ; pass-1 runs/request %.3f fallbacks/request %.4f"
-          % (sel, p2, rem, p1, fb))
+    fb = float((c[:, 3] & np.uint64(0xFFFF)).sum()) / nreq
+    nt = float(((c[:, 3] >> np.uint64(16)) & np.uint64(0xFFFF)).sum()) / nreq
+    print("per request k-cycles: select %.1f (pass2 %.1f) removal %.1f ; pass-1 runs/request %.3f fallbacks/request %.4f "
+          "near-ties/request %.4f shortlist-decided selections/request %.3f full passes/request %.3f" % (sel, p2, rem, p1, fb, nt, sl, fp))
 if os.environ.get("CTR"):
     nreq = len(g.chains) * w.window
     print("per request: compared %.1f visited %.2f scanned %.1f written %.2f" % tuple(ctr.astype(np.float64).sum(0) / nreq))
@@ -72,12 +78,16 @@ if os.environ.get("PHASES3A"):
         ids = [ai * ns + s for s in range(ns)]
         sub = c[ids]
         nreq = ns * w.window
-        sel, p2, rem = (sub[:, k].astype(np.float64).sum() / nreq / 1e3 for k in range(3))
+        sel = sub[:, 0].astype(np.float64).sum() / nreq / 1e3
+        p2 = (sub[:, 1] & np.uint64((1 << 40) - 1)).astype(np.float64).sum() / nreq / 1e3
+        fp = float((sub[:, 1] >> np.uint64(40)).sum()) / nreq
+        rem = (sub[:, 2] & np.uint64((1 << 40) - 1)).astype(np.float64).sum() / nreq / 1e3
+        sl = float((sub[:, 2] >> np.uint64(40)).sum()) / nreq
         p1 = float((sub[:, 3] >> np.uint64(32)).sum()) / nreq
         fb = float((sub[:, 3] & np.uint64(0xFFFF)).sum()) / nreq
         nt = float(((sub[:, 3] >> np.uint64(16)) & np.uint64(0xFFFF)).sum()) / nreq
-        print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f near-tie %.4f per req"
-              % (a, sel, p2, rem, p1, fb, nt))
+        print("alpha %-8g select %.1f pass2 %.1f removal %.1f k-cyc/req; pass1 %.3f fallback %.4f near-tie %.4f shortlist %.3f full %.3f per req"
+              % (a, sel, p2, rem, p1, fb, nt, sl, fp))
 if os.environ.get("DUMP"):
     os.makedirs("gpurun_out", exist_ok=True)
     np.savez(os.environ["DUMP"], cycles=cyc, counters=ctr, chains=g.chains.astype(np.int64),
