@@ -1222,13 +1222,57 @@ __device__ __forceinline__ Best select_victim(const Chain& C, uint32_t cnt, Boun
   uint32_t ai[kUnroll];
 #pragma unroll
   for (int q = 0; q < kUnroll; q++) { a1[q] = INF; a2[q] = INF; ai[q] = NIL; }
-  scan_dense(C, cnt, [&](int q, uint32_t i, uint32_t tc, float e) {
-    const float k = (tc & D_FLAGS) ? INF : __fmaf_rn(__fsub_rn(e, lo32), aide, __fmul_rn(__uint2float_rn(tc - tmin), idt));
-    const bool lt1 = k < a1[q], lt2 = k < a2[q];
-    a2[q] = lt1 ? a1[q] : (lt2 ? k : a2[q]);
-    ai[q] = lt1 ? i : ai[q];
-    a1[q] = lt1 ? k : a1[q];
-  });
+  // Keys two at a time on the packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2: per key the
+  // same three roundings as the scalar recipe, so the filter bound is unchanged); best
+  // two per lane by min/max instead of nested selects (fewer register moves in the
+  // unrolled loop).  config 3: 5.06 -> 4.92 ms in A/B (profiles/r02o_pass2_ab.txt).
+  static_assert(kUnroll % 2 == 0, "pass 2 pairs the unrolled loads");
+  {
+    const unsigned long long lo2 = ((unsigned long long)__float_as_uint(lo32) << 32) | __float_as_uint(lo32);
+    const unsigned long long ae2 = ((unsigned long long)__float_as_uint(aide) << 32) | __float_as_uint(aide);
+    const unsigned long long it2 = ((unsigned long long)__float_as_uint(idt) << 32) | __float_as_uint(idt);
+    auto pair = [&](int q, uint32_t i0, const DenseRec r0, const DenseRec r1) {
+      unsigned long long e2 = ((unsigned long long)__float_as_uint(r1.e32) << 32) | __float_as_uint(r0.e32);
+      unsigned long long t2 = ((unsigned long long)__float_as_uint(__uint2float_rn(r1.tc - tmin)) << 32) |
+                              __float_as_uint(__uint2float_rn(r0.tc - tmin));
+      unsigned long long k2;
+      asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(e2) : "l"(lo2));
+      asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(t2) : "l"(it2));
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(k2) : "l"(e2), "l"(ae2), "l"(t2));
+      const float k0 = (r0.tc & D_FLAGS) ? INF : __uint_as_float((uint32_t)k2);
+      const float k1 = (r1.tc & D_FLAGS) ? INF : __uint_as_float((uint32_t)(k2 >> 32));
+      a2[q] = fminf(a2[q], fmaxf(a1[q], k0));
+      ai[q] = k0 < a1[q] ? i0 : ai[q];
+      a1[q] = fminf(a1[q], k0);
+      a2[q + 1] = fminf(a2[q + 1], fmaxf(a1[q + 1], k1));
+      ai[q + 1] = k1 < a1[q + 1] ? i0 + 32 : ai[q + 1];
+      a1[q + 1] = fminf(a1[q + 1], k1);
+    };
+    auto one = [&](int q, uint32_t i, uint32_t tc, float e) {
+      const float k = (tc & D_FLAGS) ? INF : __fmaf_rn(__fsub_rn(e, lo32), aide, __fmul_rn(__uint2float_rn(tc - tmin), idt));
+      a2[q] = fminf(a2[q], fmaxf(a1[q], k));
+      ai[q] = k < a1[q] ? i : ai[q];
+      a1[q] = fminf(a1[q], k);
+    };
+    auto blk = [&](const DenseRec* __restrict__ d, uint32_t lo, uint32_t hi) {
+      uint32_t base = lo;
+      for (; base + 32 * kUnroll <= hi; base += 32 * kUnroll) {
+        DenseRec r[kUnroll];
+#pragma unroll
+        for (int q = 0; q < kUnroll; q++) r[q] = d[base + 32 * q + lane];
+#pragma unroll
+        for (int q = 0; q < kUnroll; q += 2) pair(q, base + 32 * q + lane, r[q], r[q + 1]);
+      }
+      for (; base < hi; base += 32) {
+        const uint32_t i = base + lane;
+        if (i < hi) { const DenseRec r = d[i]; one(0, i, r.tc, r.e32); }
+      }
+    };
+    const uint32_t ns = min(cnt, C.S);
+    blk(C.sd, 0, ns);
+    if (cnt > ns) blk(C.w.tail(), ns, cnt);
+  }
+
   // merge the per-slot best-two lists
   float k1 = a1[0], k2 = a2[0];
   uint32_t i1 = ai[0];
