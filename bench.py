@@ -472,12 +472,15 @@ def main():
                          "dram_gbs": (traffic / kern_avg_s / 1e9) if traffic else None,
                          "dram_frac": (traffic / kern_avg_s / 1e9 / peak) if traffic else None,
                          "traffic_probe": probe, "per_request": per_request,
-                         "note": ("latency-bound: achieved/frac count SURVEY d.3 algorithmic bytes, whose "
+                         "note": ("latency-bound: achieved/frac count SURVEY d.3 algorithmic bytes: the "
                                   f"{split['scan_13N'] / max(1, alg_bytes):.0%} scan term (13 B per live node per "
-                                  "eviction) is served from shared memory; dram_frac is the measured DRAM "
-                                  "traffic of the same launch" +
-                                  ("; frac > 1.2 means the SMEM-served scan bytes alone exceed the HBM peak, "
-                                   "not that HBM is saturated" if achieved / peak > 1.2 else ""))},
+                                  "eviction) is served from shared memory, and of the "
+                                  f"{split['compare_8c'] / max(1, alg_bytes):.0%} compare term (8 B per compared "
+                                  "token position) the positions whose edge lies on the query's own trace range "
+                                  "are skipped without loads; dram_frac is the measured DRAM traffic of the same "
+                                  "launch" +
+                                  ("; frac > 1.2 because those bytes never reach HBM, not because HBM is "
+                                   "saturated" if achieved / peak > 1.2 else ""))},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * len(gs),  # one replay_kernel launch per problem per step
